@@ -1,0 +1,263 @@
+/*
+ * gockpt.h — C ABI of the B200-native GoCkpt hot path: the multi-step overlapped
+ * checkpoint of GoCkpt (arXiv 2511.07035).
+ *
+ * Citations: "P:n" = line n of the paper's text, with its section.
+ *
+ * What one session computes (§4.2.1, §4.3.1): a checkpoint begun
+ * after training step t0 is split into K contiguous parts P_1..P_K of the
+ * fp32 optimizer shard (master params, Adam m, Adam v; §2.2). Session
+ * step i = training step t0+i (i = 1..K) captures part i at version S(t0+i-1)
+ * (the state before update t0+i) and, for i < K, the bf16 gradient G(t0+i)
+ * restricted to parts 1..i, i.e. the prefix [0, hi_i) ("the gradients
+ * corresponding to the existing checkpoints ... G_A^1 and G_AB^2"). A
+ * gradient-assisted replay applies updates t0+j .. t0+K-1 to each stale part
+ * j < K ("version 1 of part A ... gradients of part A computed in Steps
+ * N+1 and N+2 are used to update checkpoint version 3"), so the assembled host
+ * checkpoint equals the synchronous snapshot S(T), T = t0+K-1, bit for bit.
+ *
+ * The library IS the optimizer step: gck_submit launches the fused AdamW
+ * kernel whether or not a session is active, so the update's operation order
+ * is identical inside and outside sessions and identical to the host and GPU
+ * replays (normative update: DESIGN.md "Normative update").
+ *
+ * Conventions
+ *  - Every function returns gck_status; nothing throws or aborts across the
+ *    ABI. gck_last_error(ctx) gives a text for the last failure on ctx
+ *    (thread-local text for the stateless helpers: gck_last_error(NULL)).
+ *  - "device" pointers are CUDA device (or managed) addresses on cfg.device;
+ *    "host" pointers are ordinary process memory. Streams are passed as
+ *    void* holding a cudaStream_t (NULL = the legacy default stream).
+ *  - Arrays are flat and contiguous. fp32 arrays and the bf16 gradient /
+ *    param arrays must be 16-byte aligned (the PyTorch caching allocator
+ *    gives 512 B); a violation returns GCK_E_INVALID.
+ *  - One context per (process, CUDA device, optimizer shard). A context is
+ *    driven by one host thread at a time (the library's own internal
+ *    threads never touch caller memory).
+ */
+#ifndef GOCKPT_H_
+#define GOCKPT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GCK_ABI_VERSION 1u
+#define GCK_K_LIMIT 64u /* largest K a session may use */
+
+typedef enum {
+    GCK_OK = 0,
+    GCK_E_INVALID = 1,    /* bad argument: K = 0 or K > ceil(n/A), NULL or misaligned pointer, n = 0 */
+    GCK_E_PROTOCOL = 2,   /* call out of order: begin while a session/checkpoint is live,
+                             finalize before part K, plain submit inside a session */
+    GCK_E_STALE = 3,      /* submit's part/step does not match the session (part != step - t0,
+                             or not the next part) */
+    GCK_E_NOMEM = 4,      /* host or device allocation failed */
+    GCK_E_CUDA = 5,       /* a CUDA call failed; the context is poisoned */
+    GCK_E_INCOMPLETE = 6, /* a session slice never arrived; the checkpoint is discarded */
+    GCK_E_ABORTED = 7,    /* the checkpoint path failed; training continues, the session is void */
+    GCK_E_BUSY = 8,       /* gck_finalize_poll: the checkpoint is not consistent yet */
+    GCK_E_NODEVICE = 9    /* no CUDA device (the library never falls back to the CPU) */
+} gck_status;
+
+typedef struct gck_ctx gck_ctx;
+
+/* AdamW hyperparameters, binary64; every binary32 scalar the update uses is
+ * derived from these once per step (reading R7). */
+typedef struct {
+    double beta1, beta2, eps, weight_decay;
+} gck_hparams;
+
+enum { GCK_COPY_ENGINE = 0, GCK_COPY_ZEROCOPY = 1 };
+enum { GCK_REPLAY_HOST = 0, GCK_REPLAY_GPU = 1 };
+
+typedef struct {
+    uint32_t abi_version;   /* must be GCK_ABI_VERSION */
+    int32_t device;         /* CUDA device ordinal the tensors live on */
+    uint64_t n;             /* elements in this rank's optimizer shard (ZeRO-1, §4.5) */
+    uint32_t k_min, k_max;  /* session K range; sizes the HBM ring and pinned arena (1..GCK_K_LIMIT) */
+    uint32_t part_align;    /* A: partition boundaries are multiples of A elements (0 -> 1024; must be
+                               a multiple of 8) */
+    uint32_t ring_slots;    /* R: HBM staging slots, 1 or 2 (0 -> 2); R=2 double-buffers so one
+                               slot drains while the next step packs (§4.4.1) */
+    int32_t copy_mode;      /* GCK_COPY_ENGINE (cudaMemcpyAsync on a side stream) or GCK_COPY_ZEROCOPY
+                               (SM stores into mapped pinned memory) */
+    uint64_t chunk_bytes;   /* copy-engine chunk size (0 = one copy per section); P:362 uses 4 MiB */
+    uint32_t zc_ctas;       /* CTAs of the zero-copy drain kernel (0 -> 32) */
+    int32_t replay_mode;    /* GCK_REPLAY_HOST (thread pool) or GCK_REPLAY_GPU */
+    int32_t replay_threads; /* host replay threads (0 -> all cores of the affinity mask) */
+    int32_t timing;         /* 1: record CUDA events for stall / kernel / D2H times (gck_stats) */
+} gck_config;
+
+/* Caller-owned device tensors (PyTorch owns them; they must outlive the context). */
+typedef struct {
+    float *master;          /* fp32[n] master params (device) */
+    float *exp_avg;         /* fp32[n] Adam m (device) */
+    float *exp_avg_sq;      /* fp32[n] Adam v (device) */
+    uint16_t *param_bf16;   /* bf16[n] working params written as RNE(master') (device; NULL = skip) */
+} gck_tensors;
+
+/* One training step's update (§2.1: update N consumes G^N). */
+typedef struct {
+    uint64_t step;              /* training-step index s of this update */
+    uint64_t adam_t;            /* bias-correction count t(s) >= 1 (non-skipped updates up to s) */
+    double lr;                  /* learning rate of this step (schedule applied by the caller) */
+    double grad_scale;          /* multiplies the gradient (loss-scale unscale x clip coefficient; 1.0) */
+    int32_t skip;               /* 1: update skipped (overflow); state unchanged */
+    const uint16_t *grad_bf16;  /* bf16[n] gradient shard G(s) (device). In ring mode it only has to
+                                   stay valid until the stream passes this step's kernel. */
+} gck_step_args;
+
+/* The binary32 scalars one update consumes (a0). Shared by the GPU update, the
+ * host replay and the GPU replay, which is what makes them bit-identical. */
+typedef struct {
+    float b1, c1, b2, c2, bc1, bc2, lr, eps, wd, gs;  /* c = f32(1-beta), bc = f32(1-beta^t) */
+    int32_t skip;
+    uint32_t _pad;
+    uint64_t t;
+} gck_step_record;
+
+/* A consistent checkpoint S(step) of this shard, in library-owned pinned host
+ * memory, valid until gck_release ("the CPU retains the full checkpoint"). */
+typedef struct {
+    uint64_t step;              /* = T = t0 + K - 1 */
+    uint64_t n;
+    const float *master, *exp_avg, *exp_avg_sq;
+} gck_checkpoint;
+
+/* The staged (pre-replay) host bytes of the current session, for verification:
+ * part i's ranges of master/m/v hold S(t0+i-1); glog[i-1] holds G(t0+i)[0:hi_i]. */
+typedef struct {
+    uint64_t t0, n;
+    uint32_t K, _pad;
+    uint64_t lo[GCK_K_LIMIT], hi[GCK_K_LIMIT];      /* part i = [lo[i-1], hi[i-1]) */
+    const float *master, *exp_avg, *exp_avg_sq;      /* host, n each */
+    const uint16_t *glog[GCK_K_LIMIT];               /* host; glog[i-1] has hi[i-1] elements, i < K */
+} gck_staged;
+
+typedef struct {
+    uint64_t sessions, steps, session_steps;
+    uint64_t d2h_bytes;            /* bytes drained to host, all sessions */
+    double stall_ms_total;         /* slot-reuse waits on the compute stream (a4), all sessions */
+    double stall_ms_max;           /* largest single wait */
+    double kernel_ms_total;        /* fused kernel time, timed steps */
+    uint64_t kernel_launches_timed;
+    double d2h_ms_total;           /* D2H stream busy time */
+    double last_session_stall_ms, last_session_d2h_ms, last_replay_ms, last_finalize_wait_ms;
+    uint64_t last_session_d2h_bytes;
+    uint64_t gpu_launches;         /* kernels this context launched */
+    int32_t replay_threads;
+    int32_t _pad;
+} gck_stats;
+
+/* ---- context lifecycle -------------------------------------------------- */
+
+/* Validate, create the D2H stream + events, allocate the HBM staging ring
+ * (R slots sized for K in [k_min, k_max]) and the pinned host arena
+ * (12n checkpoint bytes + the gradient log; §4.4.2 "pre-register the
+ * CPU memory used as Pinned Memory"). Errors: INVALID, NOMEM, CUDA, NODEVICE. */
+gck_status gck_create(const gck_config *cfg, const gck_hparams *hp, const gck_tensors *t, gck_ctx **out);
+
+/* Waits for outstanding work, frees everything the library owns. NULL is a no-op. */
+gck_status gck_destroy(gck_ctx *ctx);
+
+/* ---- the session (BJ: begin_checkpoint(step, K), submit, finalize) ------ */
+
+/* Plan a session after step t0 with K parts (a1): parts balanced over
+ * A-element units, remainder to the earliest parts. Host-only, no GPU work.
+ * Errors: INVALID (K outside [k_min, k_max] or > ceil(n/A)), PROTOCOL (a
+ * session or an unreleased checkpoint is live). */
+gck_status gck_begin_checkpoint(gck_ctx *ctx, uint64_t t0, uint32_t K);
+
+/* Enqueue one optimizer step on `stream` (async; returns before the GPU runs).
+ * part = 0: a plain step (no session active). part = i in 1..K: session step
+ * i, requires args->step == t0 + i. Inside a session the compute stream first
+ * waits for the slot it is about to reuse to have drained (the only stall
+ * point, a4; "transmitted by blocking"), then runs the fused kernel that
+ * packs part i (pre-update) and G[0:hi_i] into the slot and applies the
+ * update (a2), then the D2H stream drains the slot into pinned memory (a3).
+ * Errors: INVALID, PROTOCOL, STALE, CUDA (kernel launch failure poisons ctx),
+ * ABORTED (the checkpoint path failed earlier; the update still ran). */
+gck_status gck_submit(gck_ctx *ctx, uint32_t part, const gck_step_args *args, void *stream);
+
+/* Wait until every slot of the session has drained. Does not replay. */
+gck_status gck_wait_drained(gck_ctx *ctx);
+
+/* Pointers to the staged pre-replay bytes (after gck_wait_drained, before
+ * gck_finalize). Errors: PROTOCOL if not drained or already replayed. */
+gck_status gck_get_staged(gck_ctx *ctx, gck_staged *out);
+
+/* Block until the checkpoint is consistent (drains complete, replay done, a5/a6)
+ * and describe it. Errors: PROTOCOL (part K not yet submitted), ABORTED, INCOMPLETE. */
+gck_status gck_finalize(gck_ctx *ctx, gck_checkpoint *out);
+
+/* Non-blocking finalize: GCK_E_BUSY while drains/replay are still running. */
+gck_status gck_finalize_poll(gck_ctx *ctx, gck_checkpoint *out);
+
+/* Return the checkpoint memory to the library; the next session may begin. */
+gck_status gck_release(gck_ctx *ctx);
+
+/* ---- references and variants -------------------------------------------- */
+
+/* Synchronous snapshot (the reference GoCkpt must equal): D2H copy of
+ * the live master/m/v, ordered after all work queued on `stream`; blocks until
+ * done. h_* are host arrays of n floats. */
+gck_status gck_sync_snapshot(gck_ctx *ctx, void *stream, float *h_master, float *h_m, float *h_v);
+
+/* GPU replay of the staged session (variant of a5): uploads the staged host
+ * bytes into the caller's device arrays d_* (n floats each) and a gradient
+ * scratch d_glog (>= sum_{i<K} hi_i bf16 elements), then runs the replay
+ * kernel on `stream`. Same per-element op sequence as the host replay. Call
+ * after gck_wait_drained and before gck_finalize. Blocks until done. */
+gck_status gck_replay_gpu(gck_ctx *ctx, void *stream, float *d_master, float *d_m, float *d_v, uint16_t *d_glog);
+
+gck_status gck_get_stats(const gck_ctx *ctx, gck_stats *out);
+const char *gck_last_error(const gck_ctx *ctx);
+
+/* ---- stateless building blocks (used by the context; exported for tests) */
+
+/* a0: binary32 scalars of update t from binary64 hyperparameters; beta^t is a
+ * left-to-right binary64 running product (reading R7). Host-only. */
+gck_status gck_make_step_record(const gck_hparams *hp, uint64_t adam_t, double lr, double grad_scale,
+                                int32_t skip, gck_step_record *out);
+
+/* a1: the K part ranges of [0, n) with alignment A; lo_hi[2i], lo_hi[2i+1] =
+ * lo_{i+1}, hi_{i+1}. Host-only. Errors: INVALID. */
+gck_status gck_plan_parts(uint64_t n, uint32_t K, uint32_t A, uint64_t *lo_hi);
+
+/* a5, host: replay a staged session in place. master/m/v: host arrays of n
+ * floats holding part j at S(t0+j-1); glog[i-1]: host bf16 array of >= hi_i
+ * elements (i = 1..K-1); recs[i-1]: StepRecord of update t0+i. Runs on
+ * `threads` threads (0 = all cores). Host-only; usable without a GPU. */
+gck_status gck_replay_host(const gck_step_record *recs, uint32_t K, const uint64_t *lo_hi, uint64_t n,
+                           float *master, float *m, float *v, const uint16_t *const *glog, int32_t threads);
+
+/* a5, GPU: the same replay on device arrays (d_glog[i-1] device pointers). Async on stream. */
+gck_status gck_replay_device(const gck_step_record *recs, uint32_t K, const uint64_t *lo_hi, uint64_t n,
+                             float *d_master, float *d_m, float *d_v, const uint16_t *const *d_glog,
+                             void *stream);
+
+/* a2 without a session: one fused AdamW step on device arrays. Async on stream. */
+gck_status gck_adamw_step(const gck_step_record *rec, uint64_t n, float *d_master, float *d_m, float *d_v,
+                          const uint16_t *d_grad, uint16_t *d_param_bf16, void *stream);
+
+/* ---- harness-only (NOT the method): seeded synthetic inputs ------------- */
+
+/* Fill d_out with the counter-hash generator of gockpt_inputs.py (DESIGN.md
+ * "Input recipe"): kind 1 = master (mode 0 flat / 1 model), 2 = exp_avg,
+ * 3 = exp_avg_sq, 4 = bf16 gradient of `step` (mode 0 uniform / 1 llm,
+ * zero_per_256). Element k gets global index offset + k. Async on stream. */
+gck_status gck_h_generate(int32_t kind, int32_t mode, uint64_t seed, uint64_t step, uint64_t offset,
+                          uint64_t n, uint32_t zero_per_256, void *d_out, void *stream);
+
+/* Query: number of CUDA devices visible (0 on a CPU-only host). */
+int32_t gck_device_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GOCKPT_H_ */
