@@ -90,6 +90,9 @@ typedef struct {
     int32_t replay_mode;    /* GCK_REPLAY_HOST (thread pool) or GCK_REPLAY_GPU */
     int32_t replay_threads; /* host replay threads (0 -> all cores of the affinity mask) */
     int32_t timing;         /* 1: record CUDA events for stall / kernel / D2H times (gck_stats) */
+    int32_t eager_replay;   /* 1: replay starts on a library thread as soon as the gradient log is
+                               complete (overlaps training); 0: replay runs inside gck_finalize
+                               (lets tests read the staged bytes first) */
 } gck_config;
 
 /* Caller-owned device tensors (PyTorch owns them; they must outlive the context). */
@@ -209,7 +212,7 @@ gck_status gck_sync_snapshot(gck_ctx *ctx, void *stream, float *h_master, float 
 
 /* GPU replay of the staged session (variant of a5): uploads the staged host
  * bytes into the caller's device arrays d_* (n floats each) and a gradient
- * scratch d_glog (>= sum_{i<K} hi_i bf16 elements), then runs the replay
+ * scratch d_glog (>= n*(K-1) bf16 elements; slices are 256-B aligned inside it), then runs the replay
  * kernel on `stream`. Same per-element op sequence as the host replay. Call
  * after gck_wait_drained and before gck_finalize. Blocks until done. */
 gck_status gck_replay_gpu(gck_ctx *ctx, void *stream, float *d_master, float *d_m, float *d_v, uint16_t *d_glog);

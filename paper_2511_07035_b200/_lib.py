@@ -1,0 +1,143 @@
+"""ctypes binding of include/gockpt.h (argument marshalling only).
+
+Every step of the hot path runs in libgockpt.so (sm_100a kernels + the C++
+runtime). This module only declares the C structs and function signatures and
+loads the in-tree library; it never computes anything of the method and never
+falls back to another implementation: if the library is missing, ``lib()``
+raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgockpt.so")
+
+ABI_VERSION = 1
+K_LIMIT = 64
+
+OK, E_INVALID, E_PROTOCOL, E_STALE, E_NOMEM, E_CUDA, E_INCOMPLETE, E_ABORTED, E_BUSY, E_NODEVICE = range(10)
+STATUS_NAMES = ["GCK_OK", "GCK_E_INVALID", "GCK_E_PROTOCOL", "GCK_E_STALE", "GCK_E_NOMEM", "GCK_E_CUDA",
+                "GCK_E_INCOMPLETE", "GCK_E_ABORTED", "GCK_E_BUSY", "GCK_E_NODEVICE"]
+COPY_ENGINE, COPY_ZEROCOPY = 0, 1
+REPLAY_HOST, REPLAY_GPU = 0, 1
+
+
+class Hparams(C.Structure):
+    _fields_ = [("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double), ("weight_decay", C.c_double)]
+
+
+class Config(C.Structure):
+    _fields_ = [("abi_version", C.c_uint32), ("device", C.c_int32), ("n", C.c_uint64),
+                ("k_min", C.c_uint32), ("k_max", C.c_uint32), ("part_align", C.c_uint32),
+                ("ring_slots", C.c_uint32), ("copy_mode", C.c_int32), ("chunk_bytes", C.c_uint64),
+                ("zc_ctas", C.c_uint32), ("replay_mode", C.c_int32), ("replay_threads", C.c_int32),
+                ("timing", C.c_int32), ("eager_replay", C.c_int32)]
+
+
+class Tensors(C.Structure):
+    _fields_ = [("master", C.c_void_p), ("exp_avg", C.c_void_p), ("exp_avg_sq", C.c_void_p),
+                ("param_bf16", C.c_void_p)]
+
+
+class StepArgs(C.Structure):
+    _fields_ = [("step", C.c_uint64), ("adam_t", C.c_uint64), ("lr", C.c_double), ("grad_scale", C.c_double),
+                ("skip", C.c_int32), ("grad_bf16", C.c_void_p)]
+
+
+class StepRecord(C.Structure):
+    _fields_ = [("b1", C.c_float), ("c1", C.c_float), ("b2", C.c_float), ("c2", C.c_float),
+                ("bc1", C.c_float), ("bc2", C.c_float), ("lr", C.c_float), ("eps", C.c_float),
+                ("wd", C.c_float), ("gs", C.c_float), ("skip", C.c_int32), ("_pad", C.c_uint32),
+                ("t", C.c_uint64)]
+
+
+class Checkpoint(C.Structure):
+    _fields_ = [("step", C.c_uint64), ("n", C.c_uint64), ("master", C.c_void_p), ("exp_avg", C.c_void_p),
+                ("exp_avg_sq", C.c_void_p)]
+
+
+class Staged(C.Structure):
+    _fields_ = [("t0", C.c_uint64), ("n", C.c_uint64), ("K", C.c_uint32), ("_pad", C.c_uint32),
+                ("lo", C.c_uint64 * K_LIMIT), ("hi", C.c_uint64 * K_LIMIT),
+                ("master", C.c_void_p), ("exp_avg", C.c_void_p), ("exp_avg_sq", C.c_void_p),
+                ("glog", C.c_void_p * K_LIMIT)]
+
+
+class Stats(C.Structure):
+    _fields_ = [("sessions", C.c_uint64), ("steps", C.c_uint64), ("session_steps", C.c_uint64),
+                ("d2h_bytes", C.c_uint64), ("stall_ms_total", C.c_double), ("stall_ms_max", C.c_double),
+                ("kernel_ms_total", C.c_double), ("kernel_launches_timed", C.c_uint64),
+                ("d2h_ms_total", C.c_double), ("last_session_stall_ms", C.c_double),
+                ("last_session_d2h_ms", C.c_double), ("last_replay_ms", C.c_double),
+                ("last_finalize_wait_ms", C.c_double), ("last_session_d2h_bytes", C.c_uint64),
+                ("gpu_launches", C.c_uint64), ("replay_threads", C.c_int32), ("_pad", C.c_int32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_ if not k.startswith("_")}
+
+
+P = C.c_void_p
+U64P = C.POINTER(C.c_uint64)
+
+# name -> (restype, argtypes); exactly the functions include/gockpt.h declares
+SIGNATURES = {
+    "gck_create": (C.c_int, [C.POINTER(Config), C.POINTER(Hparams), C.POINTER(Tensors), C.POINTER(P)]),
+    "gck_destroy": (C.c_int, [P]),
+    "gck_begin_checkpoint": (C.c_int, [P, C.c_uint64, C.c_uint32]),
+    "gck_submit": (C.c_int, [P, C.c_uint32, C.POINTER(StepArgs), P]),
+    "gck_wait_drained": (C.c_int, [P]),
+    "gck_get_staged": (C.c_int, [P, C.POINTER(Staged)]),
+    "gck_finalize": (C.c_int, [P, C.POINTER(Checkpoint)]),
+    "gck_finalize_poll": (C.c_int, [P, C.POINTER(Checkpoint)]),
+    "gck_release": (C.c_int, [P]),
+    "gck_sync_snapshot": (C.c_int, [P, P, P, P, P]),
+    "gck_replay_gpu": (C.c_int, [P, P, P, P, P, P]),
+    "gck_get_stats": (C.c_int, [P, C.POINTER(Stats)]),
+    "gck_last_error": (C.c_char_p, [P]),
+    "gck_make_step_record": (C.c_int, [C.POINTER(Hparams), C.c_uint64, C.c_double, C.c_double, C.c_int32,
+                                       C.POINTER(StepRecord)]),
+    "gck_plan_parts": (C.c_int, [C.c_uint64, C.c_uint32, C.c_uint32, U64P]),
+    "gck_replay_host": (C.c_int, [C.POINTER(StepRecord), C.c_uint32, U64P, C.c_uint64, P, P, P,
+                                  C.POINTER(P), C.c_int32]),
+    "gck_replay_device": (C.c_int, [C.POINTER(StepRecord), C.c_uint32, U64P, C.c_uint64, P, P, P,
+                                    C.POINTER(P), P]),
+    "gck_adamw_step": (C.c_int, [C.POINTER(StepRecord), C.c_uint64, P, P, P, P, P, P]),
+    "gck_h_generate": (C.c_int, [C.c_int32, C.c_int32, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
+                                 C.c_uint32, P, P]),
+    "gck_device_count": (C.c_int32, []),
+}
+
+_LIB = None
+
+
+class GckError(RuntimeError):
+    def __init__(self, status, msg):
+        self.status = status
+        name = STATUS_NAMES[status] if 0 <= status < len(STATUS_NAMES) else str(status)
+        super().__init__(f"{name}: {msg}")
+
+
+def lib() -> C.CDLL:
+    """Load the in-tree libgockpt.so (build it first with __graft_entry__.build())."""
+    global _LIB
+    if _LIB is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} is missing: run `python __graft_entry__.py` / build() "
+                              "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _LIB = L
+    return _LIB
+
+
+def check(status: int, ctx=None):
+    if status != OK:
+        msg = lib().gck_last_error(ctx)
+        raise GckError(status, msg.decode() if msg else "")
+    return status

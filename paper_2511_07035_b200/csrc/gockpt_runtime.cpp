@@ -1,0 +1,821 @@
+// libgockpt runtime: the C ABI of include/gockpt.h.
+//
+// Per context (one per process x device x ZeRO-1 shard, §4.5):
+//  - a session FSM: IDLE -> ACTIVE (begin) -> DRAINING (part K submitted) -> READY (finalize)
+//    -> IDLE (release); ABORTED when the checkpoint path fails (training continues);
+//  - an HBM staging ring of R slots; slot s = (i-1) mod R holds part i's pre-update state and
+//    the gradient prefix G(t0+i)[0:hi_i] (a2);
+//  - a low-priority D2H stream that drains each slot into library-owned pinned host memory
+//    ("background threads manage independent CUDA streams", §4.4.1; "pre-register the
+//    CPU memory used as Pinned Memory", §4.4.2) by copy engine or zero-copy stores (a3);
+//  - the slot-reuse wait on the caller's compute stream, the only stall point (a4; P:324
+//    "the remaining checkpoints are transmitted by blocking");
+//  - the host replay pool, run eagerly on a library thread as soon as the gradient log is
+//    complete, so reconstruction overlaps training (a5);
+//  - finalize returning the consistent checkpoint S(t0+K-1) (a6).
+#include <cuda_runtime.h>
+#include <sched.h>
+
+#include <atomic>
+#include <chrono>
+#include <condition_variable>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "internal.h"
+
+using gck::FusedArgs;
+using gck::ReplayArgs;
+using gck::ZcArgs;
+
+namespace {
+
+thread_local std::string g_tls_error;
+
+constexpr uint64_t kAlign = 256;
+inline uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+inline bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+gck_status set_tls(gck_status st, const std::string &msg) {
+    g_tls_error = msg;
+    return st;
+}
+
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = true;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) ok = cudaSetDevice(dev) == cudaSuccess;
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+gck_status plan_parts(uint64_t n, uint32_t K, uint32_t A, uint64_t *lo, uint64_t *hi) {
+    if (n == 0 || K == 0 || A == 0) return GCK_E_INVALID;
+    const uint64_t U = (n + A - 1) / A;
+    if (K > U) return GCK_E_INVALID;
+    const uint64_t base = U / K, rem = U % K;
+    uint64_t lo_unit = 0;
+    for (uint32_t i = 0; i < K; ++i) {
+        const uint64_t units = base + ((i < rem) ? 1 : 0);
+        const uint64_t hi_unit = lo_unit + units;
+        lo[i] = std::min<uint64_t>(lo_unit * A, n);
+        hi[i] = std::min<uint64_t>(hi_unit * A, n);
+        lo_unit = hi_unit;
+    }
+    return GCK_OK;
+}
+
+// Slot layout of session step i: [master | m | v | grad], each section 256-B aligned.
+struct SlotLayout {
+    uint64_t off_m, off_v, off_g, bytes;
+};
+SlotLayout slot_layout(uint64_t part_elems, uint64_t grad_elems) {
+    SlotLayout s;
+    const uint64_t st = align_up(part_elems * 4, kAlign);
+    s.off_m = st;
+    s.off_v = 2 * st;
+    s.off_g = 3 * st;
+    s.bytes = 3 * st + align_up(grad_elems * 2, kAlign);
+    return s;
+}
+
+void fill_record(double beta1, double beta2, double eps, double wd, double pow1, double pow2, uint64_t t,
+                 double lr, double gs, int32_t skip, gck_step_record *out) {
+    std::memset(out, 0, sizeof(*out));
+    out->b1 = (float)beta1;
+    out->c1 = (float)(1.0 - beta1);
+    out->b2 = (float)beta2;
+    out->c2 = (float)(1.0 - beta2);
+    out->bc1 = (float)(1.0 - pow1);
+    out->bc2 = (float)(1.0 - pow2);
+    out->lr = (float)lr;
+    out->eps = (float)eps;
+    out->wd = (float)wd;
+    out->gs = (float)gs;
+    out->skip = skip ? 1 : 0;
+    out->t = t;
+}
+
+}  // namespace
+
+enum class State { IDLE, ACTIVE, DRAINING, READY, ABORTED };
+
+struct gck_ctx {
+    gck_config cfg{};
+    gck_hparams hp{};
+    gck_tensors t{};
+    int num_sms = 148;
+    bool poisoned = false;
+    std::string last_error;
+
+    // HBM ring
+    char *ring = nullptr;
+    uint64_t slot_bytes = 0;
+    uint32_t R = 2;
+
+    // pinned host arena
+    char *arena = nullptr;
+    char *arena_dev = nullptr;  // device view of the mapped arena (zero-copy drain)
+    uint64_t arena_bytes = 0;
+    float *h_master = nullptr, *h_m = nullptr, *h_v = nullptr;
+    uint16_t *h_glog = nullptr;   // base of the gradient log
+    uint64_t glog_elems_cap = 0;  // capacity in bf16 elements (incl. per-slice padding)
+
+    cudaStream_t d2h = nullptr;
+    cudaEvent_t packed[2]{}, slot_free[2]{};
+    bool slot_used[2]{};
+    cudaEvent_t done[GCK_K_LIMIT]{};  // step i's slot fully drained (never re-recorded within a session)
+    cudaEvent_t ev_w0[GCK_K_LIMIT]{}, ev_w1[GCK_K_LIMIT]{}, ev_k1[GCK_K_LIMIT]{}, ev_d0[GCK_K_LIMIT]{},
+        ev_d1[GCK_K_LIMIT]{};
+
+    // session
+    State state = State::IDLE;
+    uint64_t t0 = 0;
+    uint32_t K = 0, next_part = 1;
+    uint64_t lo[GCK_K_LIMIT]{}, hi[GCK_K_LIMIT]{};
+    uint16_t *glog[GCK_K_LIMIT]{};
+    gck_step_record recs[GCK_K_LIMIT]{};
+    bool replayed = false;
+
+    // replay worker
+    std::thread worker;
+    std::mutex mu;
+    std::condition_variable cv;
+    bool worker_started = false, worker_done = false;
+    gck_status worker_status = GCK_OK;
+    double replay_ms = 0;
+    int replay_threads_used = 0;
+
+    // bias-correction power cache (left-to-right binary64 running products)
+    uint64_t pow_t = 0;
+    double pow1 = 1.0, pow2 = 1.0;
+
+    gck_stats stats{};
+
+    gck_status fail(gck_status st, const std::string &msg) {
+        last_error = msg;
+        return st;
+    }
+    gck_status cuda_fail(cudaError_t e, const char *what) {
+        poisoned = true;
+        return fail(GCK_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    }
+    void abort_session(cudaError_t e, const char *what) {
+        state = State::ABORTED;
+        last_error = std::string("checkpoint aborted: ") + what + ": " + cudaGetErrorString(e);
+    }
+
+    void record_for(uint64_t adam_t, double lr, double gs, int32_t skip, gck_step_record *out) {
+        const uint64_t tt = adam_t ? adam_t : 1;
+        if (tt < pow_t) {
+            pow_t = 0;
+            pow1 = pow2 = 1.0;
+        }
+        while (pow_t < tt) {
+            pow1 = pow1 * hp.beta1;
+            pow2 = pow2 * hp.beta2;
+            ++pow_t;
+        }
+        fill_record(hp.beta1, hp.beta2, hp.eps, hp.weight_decay, pow1, pow2, adam_t, lr, gs, skip, out);
+    }
+
+    void join_worker() {
+        if (worker.joinable()) worker.join();
+    }
+
+    // Runs on the worker thread (eager) or inside finalize.
+    void run_replay() {
+        const auto t_start = std::chrono::steady_clock::now();
+        gck_status st = GCK_OK;
+        {
+            DeviceGuard g(cfg.device);
+            if (K >= 2) {
+                cudaError_t e = cudaEventSynchronize(done[K - 2]);  // gradient log complete
+                if (e != cudaSuccess) st = GCK_E_ABORTED;
+            }
+            if (st == GCK_OK && !replayed) {
+                const uint16_t *gl[GCK_K_LIMIT];
+                for (uint32_t i = 0; i < K; ++i) gl[i] = glog[i];
+                st = gck::replay_host_impl(recs, K, lo, hi, h_master, h_m, h_v, gl, cfg.replay_threads,
+                                           &replay_threads_used);
+                replayed = (st == GCK_OK);
+            }
+            if (st == GCK_OK) {
+                cudaError_t e = cudaEventSynchronize(done[K - 1]);  // last part landed
+                if (e != cudaSuccess) st = GCK_E_ABORTED;
+            }
+        }
+        const double ms =
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+        std::lock_guard<std::mutex> lk(mu);
+        replay_ms = ms;
+        worker_status = st;
+        worker_done = true;
+        cv.notify_all();
+    }
+
+    void collect_session_timing() {
+        double stall = 0, d2h_ms = 0, kern = 0;
+        if (cfg.timing) {
+            for (uint32_t i = 0; i < K; ++i) {
+                float a = 0, b = 0, c = 0;
+                if (cudaEventElapsedTime(&a, ev_w0[i], ev_w1[i]) == cudaSuccess) {
+                    stall += a;
+                    if (a > stats.stall_ms_max) stats.stall_ms_max = a;
+                }
+                if (cudaEventElapsedTime(&b, ev_w1[i], ev_k1[i]) == cudaSuccess) {
+                    kern += b;
+                    stats.kernel_launches_timed++;
+                }
+                if (cudaEventElapsedTime(&c, ev_d0[i], ev_d1[i]) == cudaSuccess) d2h_ms += c;
+            }
+        }
+        stats.stall_ms_total += stall;
+        stats.kernel_ms_total += kern;
+        stats.d2h_ms_total += d2h_ms;
+        stats.last_session_stall_ms = stall;
+        stats.last_session_d2h_ms = d2h_ms;
+        stats.last_replay_ms = replay_ms;
+        stats.replay_threads = replay_threads_used;
+    }
+};
+
+// ------------------------------------------------------------------------------------------
+extern "C" {
+
+int32_t gck_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+const char *gck_last_error(const gck_ctx *ctx) {
+    return ctx ? ctx->last_error.c_str() : g_tls_error.c_str();
+}
+
+gck_status gck_make_step_record(const gck_hparams *hp, uint64_t adam_t, double lr, double grad_scale,
+                                int32_t skip, gck_step_record *out) {
+    if (!hp || !out) return set_tls(GCK_E_INVALID, "null argument");
+    if (!skip && adam_t == 0) return set_tls(GCK_E_INVALID, "adam_t must be >= 1 for a non-skipped update");
+    double p1 = 1.0, p2 = 1.0;
+    const uint64_t tt = adam_t ? adam_t : 1;
+    for (uint64_t k = 0; k < tt; ++k) {
+        p1 = p1 * hp->beta1;
+        p2 = p2 * hp->beta2;
+    }
+    fill_record(hp->beta1, hp->beta2, hp->eps, hp->weight_decay, p1, p2, adam_t, lr, grad_scale, skip, out);
+    return GCK_OK;
+}
+
+gck_status gck_plan_parts(uint64_t n, uint32_t K, uint32_t A, uint64_t *lo_hi) {
+    if (!lo_hi) return set_tls(GCK_E_INVALID, "null lo_hi");
+    uint64_t lo[GCK_K_LIMIT], hi[GCK_K_LIMIT];
+    if (K > GCK_K_LIMIT) return set_tls(GCK_E_INVALID, "K exceeds GCK_K_LIMIT");
+    gck_status st = plan_parts(n, K, A, lo, hi);
+    if (st != GCK_OK) return set_tls(st, "need n >= 1, A >= 1, 1 <= K <= ceil(n/A)");
+    for (uint32_t i = 0; i < K; ++i) {
+        lo_hi[2 * i] = lo[i];
+        lo_hi[2 * i + 1] = hi[i];
+    }
+    return GCK_OK;
+}
+
+static gck_status check_parts(const uint64_t *lo_hi, uint32_t K, uint64_t n) {
+    if (!lo_hi || K == 0 || K > GCK_K_LIMIT) return GCK_E_INVALID;
+    if (lo_hi[0] != 0 || lo_hi[2 * K - 1] != n) return GCK_E_INVALID;
+    for (uint32_t i = 0; i < K; ++i) {
+        if (lo_hi[2 * i] >= lo_hi[2 * i + 1]) return GCK_E_INVALID;
+        if (i + 1 < K && lo_hi[2 * i + 1] != lo_hi[2 * i + 2]) return GCK_E_INVALID;
+    }
+    return GCK_OK;
+}
+
+gck_status gck_replay_host(const gck_step_record *recs, uint32_t K, const uint64_t *lo_hi, uint64_t n,
+                           float *master, float *m, float *v, const uint16_t *const *glog, int32_t threads) {
+    if (!recs || !master || !m || !v || (K > 1 && !glog)) return set_tls(GCK_E_INVALID, "null argument");
+    if (check_parts(lo_hi, K, n) != GCK_OK) return set_tls(GCK_E_INVALID, "parts must tile [0, n) in order");
+    uint64_t lo[GCK_K_LIMIT], hi[GCK_K_LIMIT];
+    for (uint32_t i = 0; i < K; ++i) {
+        lo[i] = lo_hi[2 * i];
+        hi[i] = lo_hi[2 * i + 1];
+    }
+    for (uint32_t i = 0; i + 1 < K; ++i)
+        if (!glog[i]) return set_tls(GCK_E_INVALID, "null gradient slice");
+    return gck::replay_host_impl(recs, K, lo, hi, master, m, v, glog, threads, nullptr);
+}
+
+gck_status gck_replay_device(const gck_step_record *recs, uint32_t K, const uint64_t *lo_hi, uint64_t n,
+                             float *d_master, float *d_m, float *d_v, const uint16_t *const *d_glog,
+                             void *stream) {
+    if (!recs || !d_master || !d_m || !d_v || (K > 1 && !d_glog)) return set_tls(GCK_E_INVALID, "null argument");
+    if (check_parts(lo_hi, K, n) != GCK_OK) return set_tls(GCK_E_INVALID, "parts must tile [0, n) in order");
+    if (!aligned16(d_master) || !aligned16(d_m) || !aligned16(d_v))
+        return set_tls(GCK_E_INVALID, "state arrays must be 16-byte aligned");
+    ReplayArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.p = d_master;
+    a.m = d_m;
+    a.v = d_v;
+    a.K = K;
+    a.n_replay = (K > 1) ? lo_hi[2 * (K - 1) - 1] : 0;  // hi_{K-1}
+    for (uint32_t i = 0; i < K; ++i) {
+        a.lo[i] = lo_hi[2 * i];
+        a.hi[i] = lo_hi[2 * i + 1];
+        a.rec[i] = recs[i];
+        if (i + 1 < K) {
+            if (!d_glog[i] || !aligned16(d_glog[i]))
+                return set_tls(GCK_E_INVALID, "gradient slices must be non-null and 16-byte aligned");
+            a.glog[i] = d_glog[i];
+        }
+    }
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int e = gck::launch_replay(a, stream, sms);
+    if (e) return set_tls(GCK_E_CUDA, std::string("replay launch: ") + cudaGetErrorString((cudaError_t)e));
+    return GCK_OK;
+}
+
+gck_status gck_adamw_step(const gck_step_record *rec, uint64_t n, float *d_master, float *d_m, float *d_v,
+                          const uint16_t *d_grad, uint16_t *d_param_bf16, void *stream) {
+    if (!rec || !d_master || !d_m || !d_v || !d_grad || n == 0) return set_tls(GCK_E_INVALID, "null argument");
+    if (!aligned16(d_master) || !aligned16(d_m) || !aligned16(d_v) || !aligned16(d_grad) ||
+        (d_param_bf16 && !aligned16(d_param_bf16)))
+        return set_tls(GCK_E_INVALID, "arrays must be 16-byte aligned");
+    FusedArgs a;
+    std::memset(&a, 0, sizeof(a));
+    a.p = d_master;
+    a.m = d_m;
+    a.v = d_v;
+    a.g = d_grad;
+    a.out = d_param_bf16;
+    a.n = n;
+    a.rec = *rec;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int e = gck::launch_fused(a, false, stream, sms);
+    if (e) return set_tls(GCK_E_CUDA, std::string("fused launch: ") + cudaGetErrorString((cudaError_t)e));
+    return GCK_OK;
+}
+
+gck_status gck_h_generate(int32_t kind, int32_t mode, uint64_t seed, uint64_t step, uint64_t offset, uint64_t n,
+                          uint32_t zero_per_256, void *d_out, void *stream) {
+    if (!d_out || kind < 1 || kind > 4) return set_tls(GCK_E_INVALID, "bad generator arguments");
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    int e = gck::launch_generate(kind, mode, seed, step, offset, n, zero_per_256, d_out, stream, sms);
+    if (e) return set_tls(GCK_E_CUDA, std::string("generate launch: ") + cudaGetErrorString((cudaError_t)e));
+    return GCK_OK;
+}
+
+gck_status gck_create(const gck_config *cfg_in, const gck_hparams *hp, const gck_tensors *t, gck_ctx **out) {
+    if (!cfg_in || !hp || !t || !out) return set_tls(GCK_E_INVALID, "null argument");
+    *out = nullptr;
+    gck_config cfg = *cfg_in;
+    if (cfg.abi_version != GCK_ABI_VERSION) return set_tls(GCK_E_INVALID, "ABI version mismatch");
+    if (cfg.part_align == 0) cfg.part_align = 1024;
+    if (cfg.ring_slots == 0) cfg.ring_slots = 2;
+    if (cfg.k_min == 0) cfg.k_min = 1;
+    if (cfg.n == 0) return set_tls(GCK_E_INVALID, "n must be >= 1");
+    if (cfg.part_align % 8) return set_tls(GCK_E_INVALID, "part_align must be a multiple of 8");
+    if (cfg.k_max < cfg.k_min || cfg.k_max > GCK_K_LIMIT) return set_tls(GCK_E_INVALID, "need 1 <= k_min <= k_max <= 64");
+    if (cfg.ring_slots > 2) return set_tls(GCK_E_INVALID, "ring_slots must be 1 or 2");
+    if (cfg.copy_mode != GCK_COPY_ENGINE && cfg.copy_mode != GCK_COPY_ZEROCOPY)
+        return set_tls(GCK_E_INVALID, "bad copy_mode");
+    if (cfg.replay_mode != GCK_REPLAY_HOST) return set_tls(GCK_E_INVALID, "replay_mode: only GCK_REPLAY_HOST at finalize (GPU replay: gck_replay_gpu)");
+    if (!(hp->beta1 > 0 && hp->beta1 < 1 && hp->beta2 > 0 && hp->beta2 < 1 && hp->eps > 0 && hp->weight_decay >= 0))
+        return set_tls(GCK_E_INVALID, "hyperparameters out of range");
+    if (!t->master || !t->exp_avg || !t->exp_avg_sq) return set_tls(GCK_E_INVALID, "null state tensor");
+    if (!aligned16(t->master) || !aligned16(t->exp_avg) || !aligned16(t->exp_avg_sq) ||
+        (t->param_bf16 && !aligned16(t->param_bf16)))
+        return set_tls(GCK_E_INVALID, "state tensors must be 16-byte aligned");
+    const uint64_t U = (cfg.n + cfg.part_align - 1) / cfg.part_align;
+    if (cfg.k_min > U) return set_tls(GCK_E_INVALID, "k_min exceeds ceil(n/A)");
+    if (gck_device_count() <= 0) return set_tls(GCK_E_NODEVICE, "no CUDA device (the library has no CPU fallback)");
+
+    gck_ctx *c = new (std::nothrow) gck_ctx();
+    if (!c) return set_tls(GCK_E_NOMEM, "context allocation");
+    c->cfg = cfg;
+    c->hp = *hp;
+    c->t = *t;
+    c->R = cfg.ring_slots;
+    DeviceGuard g(cfg.device);
+    if (!g.ok) {
+        delete c;
+        return set_tls(GCK_E_CUDA, "cudaSetDevice failed");
+    }
+    cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, cfg.device);
+
+    // sizes: worst case over K in [k_min, min(k_max, U)]
+    uint64_t slot_max = 0, glog_max = 0;
+    const uint32_t kmax_eff = (uint32_t)std::min<uint64_t>(cfg.k_max, U);
+    for (uint32_t K = cfg.k_min; K <= kmax_eff; ++K) {
+        uint64_t lo[GCK_K_LIMIT], hi[GCK_K_LIMIT];
+        plan_parts(cfg.n, K, cfg.part_align, lo, hi);
+        uint64_t gsum = 0;
+        for (uint32_t i = 0; i < K; ++i) {
+            const uint64_t ghi = (i + 1 < K) ? hi[i] : 0;
+            slot_max = std::max(slot_max, slot_layout(hi[i] - lo[i], ghi).bytes);
+            gsum += align_up(ghi, 128);
+        }
+        glog_max = std::max(glog_max, gsum);
+    }
+    c->slot_bytes = slot_max;
+    c->glog_elems_cap = glog_max;
+    cudaError_t e = cudaMalloc((void **)&c->ring, c->slot_bytes * c->R);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        delete c;
+        return set_tls(GCK_E_NOMEM, "HBM staging ring allocation failed");
+    }
+    const uint64_t sec = align_up(cfg.n * 4, kAlign);
+    c->arena_bytes = 3 * sec + glog_max * 2;
+    e = cudaHostAlloc((void **)&c->arena, c->arena_bytes, cudaHostAllocPortable | cudaHostAllocMapped);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        cudaFree(c->ring);
+        delete c;
+        return set_tls(GCK_E_NOMEM, "pinned host arena allocation failed");
+    }
+    if (cudaHostGetDevicePointer((void **)&c->arena_dev, c->arena, 0) != cudaSuccess) {
+        cudaGetLastError();
+        c->arena_dev = c->arena;  // UVA: the host address is the device address
+    }
+    c->h_master = reinterpret_cast<float *>(c->arena);
+    c->h_m = reinterpret_cast<float *>(c->arena + sec);
+    c->h_v = reinterpret_cast<float *>(c->arena + 2 * sec);
+    c->h_glog = reinterpret_cast<uint16_t *>(c->arena + 3 * sec);
+
+    int least = 0, greatest = 0;
+    cudaDeviceGetStreamPriorityRange(&least, &greatest);
+    bool ok = cudaStreamCreateWithPriority(&c->d2h, cudaStreamNonBlocking, least) == cudaSuccess;
+    for (int s = 0; s < 2 && ok; ++s) {
+        ok = cudaEventCreateWithFlags(&c->packed[s], cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreateWithFlags(&c->slot_free[s], cudaEventDisableTiming) == cudaSuccess;
+    }
+    for (uint32_t i = 0; i < GCK_K_LIMIT && ok; ++i) {
+        ok = cudaEventCreateWithFlags(&c->done[i], cudaEventDisableTiming) == cudaSuccess;
+        if (ok && cfg.timing)
+            ok = cudaEventCreate(&c->ev_w0[i]) == cudaSuccess && cudaEventCreate(&c->ev_w1[i]) == cudaSuccess &&
+                 cudaEventCreate(&c->ev_k1[i]) == cudaSuccess && cudaEventCreate(&c->ev_d0[i]) == cudaSuccess &&
+                 cudaEventCreate(&c->ev_d1[i]) == cudaSuccess;
+    }
+    if (!ok) {
+        gck_destroy(c);
+        return set_tls(GCK_E_CUDA, "stream/event creation failed");
+    }
+    c->stats.replay_threads = cfg.replay_threads > 0 ? cfg.replay_threads : gck::default_threads();
+    *out = c;
+    return GCK_OK;
+}
+
+gck_status gck_destroy(gck_ctx *c) {
+    if (!c) return GCK_OK;
+    c->join_worker();
+    {
+        DeviceGuard g(c->cfg.device);
+        if (c->d2h) cudaStreamSynchronize(c->d2h);
+        for (int s = 0; s < 2; ++s) {
+            if (c->packed[s]) cudaEventDestroy(c->packed[s]);
+            if (c->slot_free[s]) cudaEventDestroy(c->slot_free[s]);
+        }
+        for (uint32_t i = 0; i < GCK_K_LIMIT; ++i) {
+            for (cudaEvent_t ev : {c->done[i], c->ev_w0[i], c->ev_w1[i], c->ev_k1[i], c->ev_d0[i], c->ev_d1[i]})
+                if (ev) cudaEventDestroy(ev);
+        }
+        if (c->d2h) cudaStreamDestroy(c->d2h);
+        if (c->ring) cudaFree(c->ring);
+        if (c->arena) cudaFreeHost(c->arena);
+    }
+    delete c;
+    return GCK_OK;
+}
+
+gck_status gck_begin_checkpoint(gck_ctx *c, uint64_t t0, uint32_t K) {
+    if (!c) return set_tls(GCK_E_INVALID, "null ctx");
+    if (c->poisoned) return c->fail(GCK_E_CUDA, "context poisoned by an earlier CUDA failure");
+    if (c->state != State::IDLE && c->state != State::ABORTED)
+        return c->fail(GCK_E_PROTOCOL, "begin_checkpoint while a session or an unreleased checkpoint is live");
+    if (K < c->cfg.k_min || K > c->cfg.k_max) return c->fail(GCK_E_INVALID, "K outside [k_min, k_max]");
+    if (c->state == State::ABORTED) {  // drain whatever the aborted session left queued
+        c->join_worker();
+        DeviceGuard g(c->cfg.device);
+        cudaStreamSynchronize(c->d2h);
+        cudaGetLastError();
+    }
+    if (plan_parts(c->cfg.n, K, c->cfg.part_align, c->lo, c->hi) != GCK_OK)
+        return c->fail(GCK_E_INVALID, "K exceeds ceil(n/A)");
+    uint64_t off = 0;
+    for (uint32_t i = 0; i < K; ++i) {
+        const uint64_t ghi = (i + 1 < K) ? c->hi[i] : 0;
+        c->glog[i] = ghi ? c->h_glog + off : nullptr;
+        off += align_up(ghi, 128);
+    }
+    if (off > c->glog_elems_cap) return c->fail(GCK_E_INVALID, "gradient log capacity exceeded");
+    c->t0 = t0;
+    c->K = K;
+    c->next_part = 1;
+    c->replayed = false;
+    c->worker_started = c->worker_done = false;
+    c->worker_status = GCK_OK;
+    c->replay_ms = 0;
+    c->stats.last_session_d2h_bytes = 0;
+    c->state = State::ACTIVE;
+    return GCK_OK;
+}
+
+static gck_status enqueue_drain(gck_ctx *c, uint32_t i, const SlotLayout &L, char *slot) {
+    // a3: slot -> host ckpt arrays at offset lo_i, gradient -> glog[i]
+    cudaError_t e;
+    const uint64_t lo = c->lo[i - 1], pe = c->hi[i - 1] - lo;
+    const uint64_t ghi = (i < c->K) ? c->hi[i - 1] : 0;
+    const void *src[4] = {slot, slot + L.off_m, slot + L.off_v, slot + L.off_g};
+    void *dst[4] = {c->h_master + lo, c->h_m + lo, c->h_v + lo, c->glog[i - 1]};
+    const uint64_t bytes[4] = {pe * 4, pe * 4, pe * 4, ghi * 2};
+    if (c->cfg.copy_mode == GCK_COPY_ZEROCOPY) {
+        ZcArgs z;
+        std::memset(&z, 0, sizeof(z));
+        for (int k = 0; k < 4; ++k) {
+            if (!bytes[k]) continue;
+            z.src[z.count] = src[k];
+            z.dst[z.count] = c->arena_dev + ((char *)dst[k] - c->arena);
+            z.bytes[z.count] = bytes[k];
+            z.count++;
+        }
+        if (gck::launch_zerocopy_drain(z, (int)c->cfg.zc_ctas, c->d2h)) return GCK_E_ABORTED;
+        c->stats.gpu_launches++;
+    } else {
+        const uint64_t chunk = c->cfg.chunk_bytes ? c->cfg.chunk_bytes : ~0ull;
+        for (int k = 0; k < 4; ++k) {
+            for (uint64_t o = 0; o < bytes[k]; o += chunk) {
+                const uint64_t len = std::min(chunk, bytes[k] - o);
+                e = cudaMemcpyAsync((char *)dst[k] + o, (const char *)src[k] + o, len, cudaMemcpyDeviceToHost,
+                                    c->d2h);
+                if (e != cudaSuccess) return GCK_E_ABORTED;
+            }
+        }
+    }
+    const uint64_t tot = bytes[0] + bytes[1] + bytes[2] + bytes[3];
+    c->stats.d2h_bytes += tot;
+    c->stats.last_session_d2h_bytes += tot;
+    return GCK_OK;
+}
+
+gck_status gck_submit(gck_ctx *c, uint32_t part, const gck_step_args *a, void *stream) {
+    if (!c) return set_tls(GCK_E_INVALID, "null ctx");
+    if (!a || !a->grad_bf16) return c->fail(GCK_E_INVALID, "null step args or gradient");
+    if (!aligned16(a->grad_bf16)) return c->fail(GCK_E_INVALID, "gradient must be 16-byte aligned");
+    if (c->poisoned) return c->fail(GCK_E_CUDA, "context poisoned by an earlier CUDA failure");
+    if (!a->skip && a->adam_t == 0) return c->fail(GCK_E_INVALID, "adam_t must be >= 1");
+    const bool in_session = (c->state == State::ACTIVE);
+    if (part == 0 && in_session) return c->fail(GCK_E_PROTOCOL, "plain submit inside an active session");
+    if (part != 0) {
+        if (!in_session) return c->fail(c->state == State::ABORTED ? GCK_E_ABORTED : GCK_E_PROTOCOL,
+                                        "session submit without an active session");
+        if (part != c->next_part || a->step != c->t0 + part)
+            return c->fail(GCK_E_STALE, "part must be the next part and step == t0 + part");
+    }
+    DeviceGuard g(c->cfg.device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    gck_step_record rec;
+    c->record_for(a->adam_t, a->lr, a->grad_scale, a->skip, &rec);
+
+    FusedArgs f;
+    std::memset(&f, 0, sizeof(f));
+    f.p = c->t.master;
+    f.m = c->t.exp_avg;
+    f.v = c->t.exp_avg_sq;
+    f.g = a->grad_bf16;
+    f.out = c->t.param_bf16;
+    f.n = c->cfg.n;
+    f.rec = rec;
+    c->stats.steps++;
+
+    if (part == 0) {
+        int e = gck::launch_fused(f, false, s, c->num_sms);
+        if (e) return c->cuda_fail((cudaError_t)e, "fused kernel launch");
+        c->stats.gpu_launches++;
+        return GCK_OK;
+    }
+
+    const uint32_t i = part, slot_idx = (i - 1) % c->R;
+    const uint64_t lo = c->lo[i - 1], hi = c->hi[i - 1];
+    const uint64_t ghi = (i < c->K) ? hi : 0;
+    const SlotLayout L = slot_layout(hi - lo, ghi);
+    char *slot = c->ring + (uint64_t)slot_idx * c->slot_bytes;
+    cudaError_t e = cudaSuccess;
+    bool ck_ok = true;
+    // a4: the only stall point — wait until this slot's previous contents have drained
+    if (c->cfg.timing) cudaEventRecord(c->ev_w0[i - 1], s);
+    if (c->slot_used[slot_idx]) {
+        e = cudaStreamWaitEvent(s, c->slot_free[slot_idx], 0);
+        if (e != cudaSuccess) ck_ok = false;
+    }
+    if (c->cfg.timing) cudaEventRecord(c->ev_w1[i - 1], s);
+    // a2: fused AdamW + pack
+    if (ck_ok) {
+        f.lo = lo;
+        f.hi = hi;
+        f.ghi = ghi;
+        f.sp = reinterpret_cast<float *>(slot);
+        f.sm = reinterpret_cast<float *>(slot + L.off_m);
+        f.sv = reinterpret_cast<float *>(slot + L.off_v);
+        f.sg = reinterpret_cast<uint16_t *>(slot + L.off_g);
+    }
+    int le = gck::launch_fused(f, ck_ok, s, c->num_sms);
+    if (le) return c->cuda_fail((cudaError_t)le, "fused kernel launch");
+    c->stats.gpu_launches++;
+    c->stats.session_steps++;
+    if (c->cfg.timing) cudaEventRecord(c->ev_k1[i - 1], s);
+    if (!ck_ok) {
+        c->abort_session(e, "slot wait");
+        return GCK_E_ABORTED;
+    }
+    c->recs[i - 1] = rec;
+    // a3: drain on the side stream after the pack
+    if ((e = cudaEventRecord(c->packed[slot_idx], s)) != cudaSuccess ||
+        (e = cudaStreamWaitEvent(c->d2h, c->packed[slot_idx], 0)) != cudaSuccess) {
+        c->abort_session(e, "pack event");
+        return GCK_E_ABORTED;
+    }
+    if (c->cfg.timing) cudaEventRecord(c->ev_d0[i - 1], c->d2h);
+    if (enqueue_drain(c, i, L, slot) != GCK_OK) {
+        c->abort_session(cudaGetLastError(), "drain enqueue");
+        return GCK_E_ABORTED;
+    }
+    if (c->cfg.timing) cudaEventRecord(c->ev_d1[i - 1], c->d2h);
+    if ((e = cudaEventRecord(c->slot_free[slot_idx], c->d2h)) != cudaSuccess ||
+        (e = cudaEventRecord(c->done[i - 1], c->d2h)) != cudaSuccess) {
+        c->abort_session(e, "drain event");
+        return GCK_E_ABORTED;
+    }
+    c->slot_used[slot_idx] = true;
+    c->next_part++;
+    if (i == c->K) {
+        c->state = State::DRAINING;
+        c->stats.sessions++;
+        if (c->cfg.eager_replay) {
+            c->worker_started = true;
+            c->worker = std::thread([c]() { c->run_replay(); });
+        }
+    }
+    return GCK_OK;
+}
+
+gck_status gck_wait_drained(gck_ctx *c) {
+    if (!c) return set_tls(GCK_E_INVALID, "null ctx");
+    if (c->state == State::ABORTED) return c->fail(GCK_E_ABORTED, c->last_error);
+    if (c->state != State::DRAINING && c->state != State::READY)
+        return c->fail(GCK_E_PROTOCOL, "wait_drained before part K was submitted");
+    DeviceGuard g(c->cfg.device);
+    cudaError_t e = cudaEventSynchronize(c->done[c->K - 1]);
+    if (e != cudaSuccess) return c->cuda_fail(e, "drain");
+    return GCK_OK;
+}
+
+gck_status gck_get_staged(gck_ctx *c, gck_staged *out) {
+    if (!c || !out) return set_tls(GCK_E_INVALID, "null argument");
+    if (c->state != State::DRAINING || c->worker_started || c->replayed)
+        return c->fail(GCK_E_PROTOCOL, "staged bytes are only visible between part K and finalize with eager_replay=0");
+    if (cudaEventQuery(c->done[c->K - 1]) != cudaSuccess) return c->fail(GCK_E_PROTOCOL, "call gck_wait_drained first");
+    std::memset(out, 0, sizeof(*out));
+    out->t0 = c->t0;
+    out->n = c->cfg.n;
+    out->K = c->K;
+    for (uint32_t i = 0; i < c->K; ++i) {
+        out->lo[i] = c->lo[i];
+        out->hi[i] = c->hi[i];
+        out->glog[i] = c->glog[i];
+    }
+    out->master = c->h_master;
+    out->exp_avg = c->h_m;
+    out->exp_avg_sq = c->h_v;
+    return GCK_OK;
+}
+
+static gck_status finalize_impl(gck_ctx *c, gck_checkpoint *out, bool block) {
+    if (!c || !out) return set_tls(GCK_E_INVALID, "null argument");
+    if (c->state == State::ABORTED) return c->fail(GCK_E_ABORTED, c->last_error);
+    if (c->state == State::ACTIVE || c->state == State::IDLE)
+        return c->fail(GCK_E_PROTOCOL, "finalize before part K was submitted");
+    if (c->state == State::DRAINING) {
+        const auto t_start = std::chrono::steady_clock::now();
+        if (!c->worker_started) {
+            if (!block) {
+                c->worker_started = true;
+                c->worker = std::thread([c]() { c->run_replay(); });
+                return GCK_E_BUSY;
+            }
+            c->worker_started = true;
+            c->run_replay();
+        } else {
+            std::unique_lock<std::mutex> lk(c->mu);
+            if (!block && !c->worker_done) return GCK_E_BUSY;
+            c->cv.wait(lk, [c] { return c->worker_done; });
+        }
+        c->join_worker();
+        c->stats.last_finalize_wait_ms =
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+        if (c->worker_status != GCK_OK) {
+            c->state = State::ABORTED;
+            return c->fail(c->worker_status, "replay or drain failed");
+        }
+        {
+            DeviceGuard g(c->cfg.device);
+            c->collect_session_timing();
+        }
+        c->state = State::READY;
+    }
+    out->step = c->t0 + c->K - 1;
+    out->n = c->cfg.n;
+    out->master = c->h_master;
+    out->exp_avg = c->h_m;
+    out->exp_avg_sq = c->h_v;
+    return GCK_OK;
+}
+
+gck_status gck_finalize(gck_ctx *c, gck_checkpoint *out) { return finalize_impl(c, out, true); }
+gck_status gck_finalize_poll(gck_ctx *c, gck_checkpoint *out) { return finalize_impl(c, out, false); }
+
+gck_status gck_release(gck_ctx *c) {
+    if (!c) return set_tls(GCK_E_INVALID, "null ctx");
+    if (c->state != State::READY && c->state != State::ABORTED)
+        return c->fail(GCK_E_PROTOCOL, "release without a finalized checkpoint");
+    c->join_worker();
+    c->state = State::IDLE;
+    return GCK_OK;
+}
+
+gck_status gck_sync_snapshot(gck_ctx *c, void *stream, float *h_master, float *h_m, float *h_v) {
+    if (!c || !h_master || !h_m || !h_v) return set_tls(GCK_E_INVALID, "null argument");
+    DeviceGuard g(c->cfg.device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const uint64_t b = c->cfg.n * 4;
+    cudaError_t e;
+    if ((e = cudaMemcpyAsync(h_master, c->t.master, b, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(h_m, c->t.exp_avg, b, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(h_v, c->t.exp_avg_sq, b, cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+        (e = cudaStreamSynchronize(s)) != cudaSuccess)
+        return c->cuda_fail(e, "sync snapshot");
+    return GCK_OK;
+}
+
+gck_status gck_replay_gpu(gck_ctx *c, void *stream, float *d_master, float *d_m, float *d_v, uint16_t *d_glog) {
+    if (!c || !d_master || !d_m || !d_v || !d_glog) return set_tls(GCK_E_INVALID, "null argument");
+    if (c->state != State::DRAINING || c->worker_started || c->replayed)
+        return c->fail(GCK_E_PROTOCOL, "gck_replay_gpu needs the staged bytes (eager_replay=0, before finalize)");
+    if (!aligned16(d_master) || !aligned16(d_m) || !aligned16(d_v) || !aligned16(d_glog))
+        return c->fail(GCK_E_INVALID, "device arrays must be 16-byte aligned");
+    DeviceGuard g(c->cfg.device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaEventSynchronize(c->done[c->K - 1]);
+    const uint64_t b = c->cfg.n * 4;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_master, c->h_master, b, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_m, c->h_m, b, cudaMemcpyHostToDevice, s);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_v, c->h_v, b, cudaMemcpyHostToDevice, s);
+    const uint16_t *dg[GCK_K_LIMIT] = {};
+    uint64_t off = 0;
+    for (uint32_t i = 0; i + 1 < c->K && e == cudaSuccess; ++i) {
+        dg[i] = d_glog + off;
+        e = cudaMemcpyAsync(d_glog + off, c->glog[i], c->hi[i] * 2, cudaMemcpyHostToDevice, s);
+        off += align_up(c->hi[i], 128);
+    }
+    if (e != cudaSuccess) return c->cuda_fail(e, "replay_gpu upload");
+    uint64_t lo_hi[2 * GCK_K_LIMIT];
+    for (uint32_t i = 0; i < c->K; ++i) {
+        lo_hi[2 * i] = c->lo[i];
+        lo_hi[2 * i + 1] = c->hi[i];
+    }
+    gck_status st = gck_replay_device(c->recs, c->K, lo_hi, c->cfg.n, d_master, d_m, d_v, dg, stream);
+    if (st != GCK_OK) return c->fail(st, g_tls_error);
+    c->stats.gpu_launches++;
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) return c->cuda_fail(e, "replay_gpu");
+    return GCK_OK;
+}
+
+gck_status gck_get_stats(const gck_ctx *c, gck_stats *out) {
+    if (!c || !out) return set_tls(GCK_E_INVALID, "null argument");
+    *out = c->stats;
+    return GCK_OK;
+}
+
+}  // extern "C"

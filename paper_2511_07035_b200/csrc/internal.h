@@ -1,0 +1,56 @@
+// Internal declarations shared by the runtime (gockpt_runtime.cpp), the host
+// replay (replay_host.cpp) and the sm_100a kernels (kernels.cu). Not part of the ABI.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+
+#include "gockpt.h"
+
+namespace gck {
+
+// Arguments of one fused AdamW(+pack) launch (a2).
+struct FusedArgs {
+    float *p, *m, *v;            // live state (device)
+    const uint16_t *g;           // bf16 gradient (device)
+    uint16_t *out;               // bf16 working copy (device, nullable)
+    uint64_t n;
+    gck_step_record rec;
+    // pack (session steps only): pre-update [lo, hi) -> slot state, g[0:ghi) -> slot grad
+    uint64_t lo, hi, ghi;
+    float *sp, *sm, *sv;
+    uint16_t *sg;
+};
+
+// Arguments of one replay launch (a5, GPU).
+struct ReplayArgs {
+    float *p, *m, *v;
+    uint64_t n_replay;                        // = hi_{K-1}: elements of parts 1..K-1
+    uint32_t K;
+    uint64_t lo[GCK_K_LIMIT], hi[GCK_K_LIMIT];
+    const uint16_t *glog[GCK_K_LIMIT];
+    gck_step_record rec[GCK_K_LIMIT];
+};
+
+// Up to 4 (src, dst, bytes) sections drained by the zero-copy kernel (a3 variant).
+struct ZcArgs {
+    const void *src[4];
+    void *dst[4];
+    uint64_t bytes[4];
+    int count;
+};
+
+// Launchers (kernels.cu). Return the cudaError_t as int (0 = success).
+int launch_fused(const FusedArgs &a, bool pack, void *stream, int num_sms);
+int launch_replay(const ReplayArgs &a, void *stream, int num_sms);
+int launch_zerocopy_drain(const ZcArgs &a, int ctas, void *stream);
+int launch_generate(int kind, int mode, uint64_t seed, uint64_t step, uint64_t offset, uint64_t n,
+                    uint32_t zero_per_256, void *out, void *stream, int num_sms);
+
+// Host replay (replay_host.cpp).
+gck_status replay_host_impl(const gck_step_record *recs, uint32_t K, const uint64_t *lo, const uint64_t *hi,
+                            float *p, float *m, float *v, const uint16_t *const *glog, int threads,
+                            int *threads_used);
+int default_threads();
+
+}  // namespace gck

@@ -1,0 +1,132 @@
+// Host replay engine (a5): the CPU reconstruction phase of GoCkpt, §4.3.1
+// ("we update parameters on the CPU using the AdamW optimization strategy ... we also use
+// a multi-threading mechanism to update the parameters in parallel").
+//
+// Every stale part j < K is brought from S(t0+j-1) to S(t0+K-1) by applying updates
+// t0+j .. t0+K-1 in ascending order with the recorded gradients and StepRecords. The
+// per-element op sequence is the normative update, identical to the sm_100a
+// kernels, so the result is bit-identical to the GPU's synchronous snapshot.
+//
+// Build flags that the bit-exactness depends on (see build.py): -ffp-contract=off (no FMA
+// contraction), no -ffast-math, -fno-math-errno (lets GCC vectorise sqrtf; IEEE sqrt is
+// unchanged). Each worker clears MXCSR.FTZ/DAZ (denormals are kept, reading R13).
+//
+// Traffic: the batch order streams each stale element once (load p, m, v; K-j updates
+// in L1; store), i.e. 24 B + 2 B per pending step, the minimum for a batch replay.
+#include <pthread.h>
+#include <sched.h>
+#include <xmmintrin.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <thread>
+#include <vector>
+
+#include "internal.h"
+
+namespace gck {
+namespace {
+
+constexpr int kBlock = 1024;            // elements kept hot in L1 across the K-j updates (12 KiB)
+constexpr uint64_t kTask = 1ull << 16;  // elements per scheduling task
+
+struct Rec {
+    float b1, c1, b2, c2, bc1, bc2, lr, eps, wd, gs;
+};
+
+// One update over cnt contiguous elements. The loop is vectorised (AVX-512 / AVX2 clones);
+// vdivps / vsqrtps are correctly rounded, and -ffp-contract=off keeps every * and + separate.
+__attribute__((target_clones("avx512f", "avx2", "default"))) void update_block(
+    float *__restrict p, float *__restrict m, float *__restrict v, const uint16_t *__restrict g, int cnt,
+    const Rec &r) {
+    for (int e = 0; e < cnt; ++e) {
+        const uint32_t bits = (uint32_t)g[e] << 16;
+        float gf;
+        std::memcpy(&gf, &bits, 4);
+        gf = gf * r.gs;
+        const float mm = (r.b1 * m[e]) + (r.c1 * gf);
+        const float vv = (r.b2 * v[e]) + (r.c2 * (gf * gf));
+        const float mh = mm / r.bc1;
+        const float vh = vv / r.bc2;
+        const float u = mh / (__builtin_sqrtf(vh) + r.eps);
+        p[e] = p[e] - (r.lr * (u + (r.wd * p[e])));
+        m[e] = mm;
+        v[e] = vv;
+    }
+}
+
+struct Task {
+    uint32_t j;  // 0-based part index
+    uint64_t a, b;
+};
+
+void clear_ftz_daz() {
+    // MXCSR bits: 15 = FTZ, 6 = DAZ; rounding control 13-14 = 00 (nearest)
+    unsigned csr = _mm_getcsr();
+    csr &= ~((1u << 15) | (1u << 6) | (3u << 13));
+    _mm_setcsr(csr);
+}
+
+}  // namespace
+
+int default_threads() {
+    cpu_set_t set;
+    CPU_ZERO(&set);
+    if (sched_getaffinity(0, sizeof(set), &set) == 0) {
+        const int c = CPU_COUNT(&set);
+        if (c > 0) return c;
+    }
+    const unsigned h = std::thread::hardware_concurrency();
+    return h ? (int)h : 1;
+}
+
+gck_status replay_host_impl(const gck_step_record *recs, uint32_t K, const uint64_t *lo, const uint64_t *hi,
+                            float *p, float *m, float *v, const uint16_t *const *glog, int threads,
+                            int *threads_used) {
+    if (K <= 1) {
+        if (threads_used) *threads_used = 0;
+        return GCK_OK;
+    }
+    std::vector<Rec> rr(K);
+    for (uint32_t i = 0; i < K; ++i)
+        rr[i] = Rec{recs[i].b1, recs[i].c1, recs[i].b2, recs[i].c2, recs[i].bc1, recs[i].bc2,
+                    recs[i].lr, recs[i].eps, recs[i].wd, recs[i].gs};
+    // tasks, heaviest first (part j carries K-1-j pending updates)
+    std::vector<Task> tasks;
+    for (uint32_t j = 0; j + 1 < K; ++j)
+        for (uint64_t a = lo[j]; a < hi[j]; a += kTask) tasks.push_back(Task{j, a, std::min(hi[j], a + kTask)});
+    std::stable_sort(tasks.begin(), tasks.end(), [](const Task &x, const Task &y) { return x.j < y.j; });
+    if (threads <= 0) threads = default_threads();
+    threads = (int)std::min<uint64_t>((uint64_t)threads, std::max<uint64_t>(1, tasks.size()));
+    if (threads_used) *threads_used = threads;
+    std::atomic<uint64_t> next{0};
+    auto worker = [&]() {
+        const unsigned saved_csr = _mm_getcsr();
+        clear_ftz_daz();
+        for (;;) {
+            const uint64_t t = next.fetch_add(1, std::memory_order_relaxed);
+            if (t >= tasks.size()) break;
+            const Task &tk = tasks[t];
+            for (uint64_t b0 = tk.a; b0 < tk.b; b0 += kBlock) {
+                const int cnt = (int)std::min<uint64_t>(kBlock, tk.b - b0);
+                for (uint32_t i = tk.j; i + 1 < K; ++i) {  // updates t0+j+1 .. t0+K-1 (1-based parts)
+                    if (recs[i].skip) continue;
+                    update_block(p + b0, m + b0, v + b0, glog[i] + b0, cnt, rr[i]);
+                }
+            }
+        }
+        _mm_setcsr(saved_csr);
+    };
+    if (threads == 1) {
+        worker();
+    } else {
+        std::vector<std::thread> pool;
+        pool.reserve(threads);
+        for (int k = 0; k < threads; ++k) pool.emplace_back(worker);
+        for (auto &th : pool) th.join();
+    }
+    return GCK_OK;
+}
+
+}  // namespace gck

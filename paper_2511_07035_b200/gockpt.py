@@ -1,0 +1,217 @@
+"""Python face of libgockpt (same names as include/gockpt.h; marshalling only).
+
+PyTorch supplies device memory and streams; every step of the hot path runs
+in the library. Host results are returned as numpy views of library-owned
+pinned memory (no copy), valid until ``release()``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib as L
+from ._lib import check, lib
+
+
+def _stream_ptr(stream) -> int | None:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def _dptr(t) -> int | None:
+    if t is None:
+        return None
+    if not t.is_cuda or not t.is_contiguous():
+        raise ValueError("expected a contiguous CUDA tensor")
+    return t.data_ptr()
+
+
+def _np_view(ptr: int, n: int, dtype) -> np.ndarray:
+    if n == 0:
+        return np.zeros(0, dtype=dtype)
+    ctype = {np.float32: C.c_float, np.uint16: C.c_uint16}[dtype]
+    return np.ctypeslib.as_array((ctype * n).from_address(ptr))
+
+
+def _host_ptr(a: np.ndarray, dtype) -> int:
+    if a.dtype != dtype or not a.flags["C_CONTIGUOUS"]:
+        raise ValueError(f"expected a contiguous {np.dtype(dtype).name} array")
+    return a.ctypes.data
+
+
+# ----------------------------------------------------------------------------- stateless
+def make_step_record(beta1, beta2, eps, weight_decay, adam_t, lr, grad_scale=1.0, skip=False) -> L.StepRecord:
+    """a0 (gck_make_step_record)."""
+    hp = L.Hparams(beta1, beta2, eps, weight_decay)
+    rec = L.StepRecord()
+    check(lib().gck_make_step_record(C.byref(hp), adam_t, lr, grad_scale, int(skip), C.byref(rec)))
+    return rec
+
+
+def plan_parts(n: int, K: int, A: int = 1024):
+    """a1 (gck_plan_parts) -> [(lo, hi), ...]."""
+    buf = (C.c_uint64 * (2 * K))()
+    check(lib().gck_plan_parts(n, K, A, buf))
+    return [(buf[2 * i], buf[2 * i + 1]) for i in range(K)]
+
+
+def _recs_array(recs):
+    arr = (L.StepRecord * len(recs))()
+    for i, r in enumerate(recs):
+        arr[i] = r
+    return arr
+
+
+def _parts_array(parts):
+    buf = (C.c_uint64 * (2 * len(parts)))()
+    for i, (lo, hi) in enumerate(parts):
+        buf[2 * i], buf[2 * i + 1] = lo, hi
+    return buf
+
+
+def replay_host(recs, parts, master: np.ndarray, m: np.ndarray, v: np.ndarray, glog, threads: int = 0):
+    """a5 host (gck_replay_host), in place on numpy float32 arrays; glog[i-1] uint16 arrays."""
+    K = len(parts)
+    gl = (C.c_void_p * max(1, K))()
+    for i, g in enumerate(glog):
+        gl[i] = _host_ptr(g, np.uint16)
+    check(lib().gck_replay_host(_recs_array(recs), K, _parts_array(parts), len(master),
+                                _host_ptr(master, np.float32), _host_ptr(m, np.float32),
+                                _host_ptr(v, np.float32), gl, threads))
+
+
+def replay_device(recs, parts, d_master, d_m, d_v, d_glog, stream=None):
+    """a5 GPU (gck_replay_device), in place on CUDA tensors; d_glog[i-1] uint16/int16 CUDA tensors."""
+    K = len(parts)
+    gl = (C.c_void_p * max(1, K))()
+    for i, g in enumerate(d_glog):
+        gl[i] = _dptr(g)
+    check(lib().gck_replay_device(_recs_array(recs), K, _parts_array(parts), d_master.numel(), _dptr(d_master),
+                                  _dptr(d_m), _dptr(d_v), gl, _stream_ptr(stream)))
+
+
+def adamw_step(rec, d_master, d_m, d_v, d_grad, d_param_bf16=None, stream=None):
+    """a2 without a session (gck_adamw_step)."""
+    check(lib().gck_adamw_step(C.byref(rec), d_master.numel(), _dptr(d_master), _dptr(d_m), _dptr(d_v),
+                               _dptr(d_grad), _dptr(d_param_bf16), _stream_ptr(stream)))
+
+
+GEN_MASTER, GEN_EXP_AVG, GEN_EXP_AVG_SQ, GEN_GRAD = 1, 2, 3, 4
+
+
+def h_generate(kind, out, seed, step=0, offset=0, mode=0, zero_per_256=4, stream=None):
+    """Harness only: fill a CUDA tensor with the gockpt_inputs.py generator (gck_h_generate)."""
+    check(lib().gck_h_generate(kind, mode, seed, step, offset, out.numel(), zero_per_256, _dptr(out),
+                               _stream_ptr(stream)))
+
+
+def device_count() -> int:
+    return int(lib().gck_device_count())
+
+
+# ----------------------------------------------------------------------------- context
+@dataclass
+class HostCheckpoint:
+    step: int
+    master: np.ndarray
+    exp_avg: np.ndarray
+    exp_avg_sq: np.ndarray
+
+
+class GoCkpt:
+    """One GoCkpt context over a caller-owned fp32 optimizer shard (gck_create ... gck_destroy)."""
+
+    def __init__(self, master, exp_avg, exp_avg_sq, param_bf16=None, *, beta1=0.9, beta2=0.999, eps=1e-8,
+                 weight_decay=0.01, k_min=1, k_max=8, part_align=1024, ring_slots=2, copy_mode="ce",
+                 chunk_bytes=0, zc_ctas=0, replay_threads=0, timing=True, eager_replay=True):
+        n = master.numel()
+        if exp_avg.numel() != n or exp_avg_sq.numel() != n or (param_bf16 is not None and param_bf16.numel() != n):
+            raise ValueError("state tensors must have the same number of elements")
+        self.n = n
+        self._keep = (master, exp_avg, exp_avg_sq, param_bf16)
+        cfg = L.Config(L.ABI_VERSION, master.device.index or 0, n, k_min, k_max, part_align, ring_slots,
+                       {"ce": L.COPY_ENGINE, "zerocopy": L.COPY_ZEROCOPY}[copy_mode], chunk_bytes, zc_ctas,
+                       L.REPLAY_HOST, replay_threads, int(timing), int(eager_replay))
+        hp = L.Hparams(beta1, beta2, eps, weight_decay)
+        self.hparams = dict(beta1=beta1, beta2=beta2, eps=eps, weight_decay=weight_decay)
+        t = L.Tensors(_dptr(master), _dptr(exp_avg), _dptr(exp_avg_sq), _dptr(param_bf16))
+        ctx = C.c_void_p()
+        check(lib().gck_create(C.byref(cfg), C.byref(hp), C.byref(t), C.byref(ctx)))
+        self._ctx = ctx
+
+    # -- session
+    def begin_checkpoint(self, t0: int, K: int):
+        check(lib().gck_begin_checkpoint(self._ctx, t0, K), self._ctx)
+
+    def submit(self, part: int, step: int, adam_t: int, lr: float, grad, grad_scale: float = 1.0,
+               skip: bool = False, stream=None) -> int:
+        a = L.StepArgs(step, adam_t, lr, grad_scale, int(skip), _dptr(grad))
+        st = lib().gck_submit(self._ctx, part, C.byref(a), _stream_ptr(stream))
+        if st not in (L.OK,):
+            check(st, self._ctx)
+        return st
+
+    def wait_drained(self):
+        check(lib().gck_wait_drained(self._ctx), self._ctx)
+
+    def staged(self):
+        s = L.Staged()
+        check(lib().gck_get_staged(self._ctx, C.byref(s)), self._ctx)
+        K, n = s.K, s.n
+        parts = [(s.lo[i], s.hi[i]) for i in range(K)]
+        glog = [_np_view(s.glog[i], parts[i][1], np.uint16) for i in range(K - 1)]
+        return dict(t0=s.t0, K=K, parts=parts, master=_np_view(s.master, n, np.float32),
+                    exp_avg=_np_view(s.exp_avg, n, np.float32), exp_avg_sq=_np_view(s.exp_avg_sq, n, np.float32),
+                    glog=glog)
+
+    def finalize(self, block: bool = True) -> HostCheckpoint | None:
+        ck = L.Checkpoint()
+        fn = lib().gck_finalize if block else lib().gck_finalize_poll
+        st = fn(self._ctx, C.byref(ck))
+        if st == L.E_BUSY:
+            return None
+        check(st, self._ctx)
+        return HostCheckpoint(ck.step, _np_view(ck.master, ck.n, np.float32),
+                              _np_view(ck.exp_avg, ck.n, np.float32), _np_view(ck.exp_avg_sq, ck.n, np.float32))
+
+    def release(self):
+        check(lib().gck_release(self._ctx), self._ctx)
+
+    # -- references / variants
+    def sync_snapshot(self, stream=None):
+        out = [np.empty(self.n, np.float32) for _ in range(3)]
+        check(lib().gck_sync_snapshot(self._ctx, _stream_ptr(stream), *[o.ctypes.data for o in out]), self._ctx)
+        return tuple(out)
+
+    def replay_gpu(self, d_master, d_m, d_v, d_glog, stream=None):
+        check(lib().gck_replay_gpu(self._ctx, _stream_ptr(stream), _dptr(d_master), _dptr(d_m), _dptr(d_v),
+                                   _dptr(d_glog)), self._ctx)
+
+    def stats(self) -> dict:
+        s = L.Stats()
+        check(lib().gck_get_stats(self._ctx, C.byref(s)))
+        return s.as_dict()
+
+    def close(self):
+        if getattr(self, "_ctx", None):
+            lib().gck_destroy(self._ctx)
+            self._ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *exc):
+        self.close()

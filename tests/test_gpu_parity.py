@@ -1,0 +1,262 @@
+"""GPU parity of the CUDA path against the oracle (-m gpu; calls go through the C ABI).
+
+Bar (BASELINE.json north_star): pack and copy bit-exact; replayed fp32 state
+bit-exact against the GPU's own synchronous snapshot; within 1e-6 max relative
+error of the CPU oracle per element (expected: 0, the op order is pinned).
+Sizes span many 2048-element tiles plus a ragged tail.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+import gockpt_inputs as gi
+import oracle
+from gpu_helpers import HP, up_f32, up_u16, down_f32, down_u16, assert_state_equal, session_inputs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def G():
+    from paper_2511_07035_b200 import build as gbuild
+    gbuild.build()
+    import paper_2511_07035_b200 as G
+    assert torch.cuda.is_available(), "the -m gpu tests need a CUDA device"
+    assert G.device_count() >= 1
+    return G
+
+
+def _make_ctx(G, state, K, **kw):
+    p, m, v = (up_f32(x) for x in state)
+    out = torch.zeros(p.numel(), dtype=torch.int16, device="cuda")
+    kw.setdefault("k_min", 1)
+    kw.setdefault("k_max", max(K, 8))
+    ctx = G.GoCkpt(p, m, v, out, **HP, **kw)
+    return ctx, (p, m, v, out)
+
+
+# ---------------------------------------------------------------- generator (harness) parity
+@pytest.mark.parametrize("n,offset", [(1, 0), (1000, 17), (1 << 20, 5_000_000_007)])
+def test_generator_matches_numpy(G, n, offset):
+    for kind, mode, fn in [(1, 0, lambda: gi.master(42, n, offset)), (1, 1, lambda: gi.master(42, n, offset, 1)),
+                           (2, 0, lambda: gi.exp_avg(42, n, offset)), (3, 0, lambda: gi.exp_avg_sq(42, n, offset))]:
+        t = torch.empty(n, dtype=torch.float32, device="cuda")
+        G.h_generate(kind, t, 42, 0, offset, mode)
+        assert np.array_equal(down_f32(t).view(np.uint32), fn().view(np.uint32)), (kind, mode)
+    for mode in (gi.GRAD_UNIFORM, gi.GRAD_LLM):
+        t = torch.empty(n, dtype=torch.int16, device="cuda")
+        G.h_generate(4, t, 7, 123, offset, mode, 4)
+        assert np.array_equal(down_u16(t), gi.grad_bits(7, 123, n, offset, mode=mode, zero_per_256=4))
+
+
+# ---------------------------------------------------------------- a2 without a session
+@pytest.mark.parametrize("n", [1, 7, 8, 2048 * 37 + 5, 1_000_003])
+def test_fused_step_trajectory_vs_oracle(G, n):
+    seed, t0, steps = 11, 50, 4
+    state, grads, recs, sargs = session_inputs(seed, n, steps, t0)
+    p, m, v = (up_f32(x) for x in state)
+    out = torch.zeros(n, dtype=torch.int16, device="cuda")
+    want = oracle.trajectory(*state, grads, recs)
+    for k in range(steps):
+        r = G.make_step_record(HP["beta1"], HP["beta2"], HP["eps"], HP["weight_decay"], sargs[k]["adam_t"],
+                               sargs[k]["lr"], sargs[k]["grad_scale"], sargs[k]["skip"])
+        G.adamw_step(r, p, m, v, up_u16(grads[k]), out)
+        torch.cuda.synchronize()
+        assert_state_equal((down_f32(p), down_f32(m), down_f32(v)), want[k + 1], f"step {k + 1}")
+        assert np.array_equal(down_u16(out), oracle.rne_bf16(want[k + 1][0]))
+
+
+# ---------------------------------------------------------------- the full session, staged + replays
+@pytest.mark.parametrize("n,K,A,R,copy", [
+    (1 << 20, 4, 1024, 2, "ce"),            # config 1
+    (1_000_003, 4, 1024, 2, "ce"),          # ragged tail
+    (1_000_003, 4, 1024, 1, "ce"),          # single slot
+    (1 << 20, 4, 1024, 2, "zerocopy"),      # zero-copy drain
+    (300_007, 8, 8, 2, "ce"),               # fine alignment, K=8
+    (5000, 5, 8, 2, "zerocopy"),
+    (64, 8, 8, 1, "ce"),                    # one unit per part
+    (1 << 20, 1, 1024, 2, "ce"),            # K=1: a plain snapshot, no gradients
+])
+@pytest.mark.parametrize("seed", [42, 7])
+def test_session_staged_replays_and_snapshot(G, n, K, A, R, copy, seed):
+    t0 = 10
+    state, grads, recs, sargs = session_inputs(seed, n, K, t0)
+    ctx, (p, m, v, out) = _make_ctx(G, state, K, part_align=A, ring_slots=R, copy_mode=copy, eager_replay=False,
+                                    chunk_bytes=(1 << 20) if copy == "ce" and R == 1 else 0)
+    parts = oracle.make_parts(n, K, A)
+    assert G.plan_parts(n, K, A) == parts
+    g_dev = [up_u16(g) for g in grads]
+    ctx.begin_checkpoint(t0, K)
+    snap = None
+    for i in range(1, K + 1):
+        if i == K:
+            snap = ctx.sync_snapshot()                   # S(T), T = t0+K-1: the reference
+        a = sargs[i - 1]
+        ctx.submit(i, a["step"], a["adam_t"], a["lr"], g_dev[i - 1], a["grad_scale"], a["skip"])
+    torch.cuda.synchronize()
+    # live state after update t0+K equals the oracle trajectory
+    traj = oracle.trajectory(*state, grads, recs)
+    assert_state_equal((down_f32(p), down_f32(m), down_f32(v)), traj[K], "live S(t0+K)")
+    assert_state_equal(snap, traj[K - 1], "sync snapshot S(T)")
+    # staged bytes == the oracle's capture (pack + copy are bit copies, V4)
+    ctx.wait_drained()
+    st = ctx.staged()
+    assert st["parts"] == parts and st["K"] == K and st["t0"] == t0
+    cap, glog, _ = oracle.capture_session(*state, grads, recs, parts)
+    assert_state_equal((st["master"], st["exp_avg"], st["exp_avg_sq"]), oracle.assemble(cap), "staged")
+    assert len(st["glog"]) == K - 1
+    for i in range(K - 1):
+        assert np.array_equal(st["glog"][i], glog[i]), f"glog {i + 1}"
+    # GPU replay (V6) == snapshot
+    dP, dM, dV = (torch.empty(n, dtype=torch.float32, device="cuda") for _ in range(3))
+    dG = torch.empty(max(1, n * (K - 1) + 128 * K), dtype=torch.int16, device="cuda")
+    ctx.replay_gpu(dP, dM, dV, dG)
+    assert_state_equal((down_f32(dP), down_f32(dM), down_f32(dV)), snap, "gpu replay vs snapshot")
+    # host replay at finalize (V5) == snapshot == oracle O2 == oracle O1 (V7)
+    ck = ctx.finalize()
+    assert ck.step == t0 + K - 1
+    assert_state_equal((ck.master, ck.exp_avg, ck.exp_avg_sq), snap, "host replay vs snapshot")
+    assert_state_equal((ck.master, ck.exp_avg, ck.exp_avg_sq), oracle.replay(cap, glog, recs, parts), "vs O2")
+    s = ctx.stats()
+    assert s["sessions"] == 1 and s["session_steps"] == K
+    assert s["d2h_bytes"] == oracle.session_bytes(parts)
+    ctx.release()
+    ctx.close()
+
+
+def test_skipped_step_inside_session(G):
+    n, K, t0 = 200_000, 4, 30
+    state, grads, recs, sargs = session_inputs(3, n, K, t0, skips={t0 + 2})
+    ctx, (p, m, v, out) = _make_ctx(G, state, K, part_align=64)
+    ctx.begin_checkpoint(t0, K)
+    g_dev = [up_u16(g) for g in grads]
+    for i in range(1, K + 1):
+        if i == K:
+            snap = ctx.sync_snapshot()
+        a = sargs[i - 1]
+        ctx.submit(i, a["step"], a["adam_t"], a["lr"], g_dev[i - 1], a["grad_scale"], a["skip"])
+    ck = ctx.finalize()
+    assert_state_equal((ck.master, ck.exp_avg, ck.exp_avg_sq), snap, "skip: host replay vs snapshot")
+    want = oracle.trajectory(*state, grads[:K - 1], recs[:K - 1])[-1]
+    assert_state_equal((ck.master, ck.exp_avg, ck.exp_avg_sq), want, "skip: vs oracle")
+    ctx.release()
+    ctx.close()
+
+
+# ---------------------------------------------------------------- eager replay, several sessions, plain steps
+def test_eager_replay_multiple_sessions_with_plain_steps(G):
+    n, K = 1 << 20, 4
+    seed = 5
+    state = gi.warm_state(seed, n)
+    p, m, v = (up_f32(x) for x in state)
+    ctx = G.GoCkpt(p, m, v, None, **HP, k_min=2, k_max=8, eager_replay=True)
+    ref = tuple(x.copy() for x in state)
+    step, t = 0, 0
+    for sess in range(3):
+        Ks = (K, 2, 8)[sess]
+        for _ in range(3):                               # plain steps between sessions
+            step += 1
+            t += 1
+            g = gi.grad_bits(seed, step, n)
+            ctx.submit(0, step, t, 1e-3, up_u16(g))
+            ref = oracle.adamw_update(*ref, g, oracle.make_step_record(t=t, lr=1e-3, **HP))[:3]
+        ctx.begin_checkpoint(step, Ks)
+        target = None
+        for i in range(1, Ks + 1):
+            step += 1
+            t += 1
+            g = gi.grad_bits(seed, step, n)
+            ctx.submit(i, step, t, 1e-3, up_u16(g))
+            ref = oracle.adamw_update(*ref, g, oracle.make_step_record(t=t, lr=1e-3, **HP))[:3]
+            if i == Ks - 1 or Ks == 1:
+                target = tuple(x.copy() for x in ref)
+        # training continues while the checkpoint completes in the background
+        step += 1
+        t += 1
+        g = gi.grad_bits(seed, step, n)
+        ctx.submit(0, step, t, 1e-3, up_u16(g))
+        ref = oracle.adamw_update(*ref, g, oracle.make_step_record(t=t, lr=1e-3, **HP))[:3]
+        ck = None
+        while ck is None:
+            ck = ctx.finalize(block=False)
+        assert ck.step == step - 2
+        assert_state_equal((ck.master, ck.exp_avg, ck.exp_avg_sq), target, f"session {sess}")
+        ctx.release()
+    torch.cuda.synchronize()
+    assert_state_equal((down_f32(p), down_f32(m), down_f32(v)), ref, "live")
+    s = ctx.stats()
+    assert s["sessions"] == 3 and s["stall_ms_total"] >= 0
+    ctx.close()
+
+
+# ---------------------------------------------------------------- torn read
+def test_scribbled_live_state_does_not_reach_the_checkpoint(G):
+    # SPEC torn-read freedom: the drain reads the slot, never live memory. Right after
+    # the last session step's kernel, overwrite the live state on the compute stream; the
+    # checkpoint must still be S(T).
+    n, K, t0 = 1 << 20, 4, 10
+    state, grads, recs, sargs = session_inputs(9, n, K, t0)
+    ctx, (p, m, v, out) = _make_ctx(G, state, K, eager_replay=True)
+    ctx.begin_checkpoint(t0, K)
+    for i in range(1, K + 1):
+        a = sargs[i - 1]
+        ctx.submit(i, a["step"], a["adam_t"], a["lr"], up_u16(grads[i - 1]), a["grad_scale"], a["skip"])
+        p.fill_(float("nan"))
+        m.fill_(-7.0)
+        v.fill_(123.0)
+        # restore the true trajectory so the next step's capture is meaningful
+        traj_i = oracle.trajectory(*state, grads[:i], recs[:i])[-1]
+        p.copy_(up_f32(traj_i[0]))
+        m.copy_(up_f32(traj_i[1]))
+        v.copy_(up_f32(traj_i[2]))
+    ck = ctx.finalize()
+    want = oracle.trajectory(*state, grads[:K - 1], recs[:K - 1])[-1]
+    assert_state_equal((ck.master, ck.exp_avg, ck.exp_avg_sq), want, "scribbled")
+    ctx.release()
+    ctx.close()
+
+
+# ---------------------------------------------------------------- protocol errors through the ABI
+def test_protocol_errors(G):
+    from paper_2511_07035_b200 import GckError
+    from paper_2511_07035_b200 import _lib as L
+    n, K, t0 = 4096, 4, 3
+    state, grads, recs, sargs = session_inputs(1, n, K, t0)
+    ctx, (p, m, v, out) = _make_ctx(G, state, K, part_align=8, k_min=2, k_max=4)
+    g = up_u16(grads[0])
+
+    def status_of(fn, *a):
+        try:
+            fn(*a)
+        except GckError as e:
+            return e.status
+        return L.OK
+
+    assert status_of(ctx.begin_checkpoint, t0, 5) == L.E_INVALID        # K > k_max
+    assert status_of(ctx.begin_checkpoint, t0, 1) == L.E_INVALID        # K < k_min
+    assert status_of(ctx.finalize) == L.E_PROTOCOL                      # no session
+    assert status_of(ctx.release) == L.E_PROTOCOL
+    assert status_of(ctx.submit, 1, t0 + 1, 1, 1e-3, g) == L.E_PROTOCOL  # session submit, no session
+    ctx.begin_checkpoint(t0, K)
+    assert status_of(ctx.begin_checkpoint, t0, K) == L.E_PROTOCOL       # begin twice
+    assert status_of(ctx.submit, 0, t0 + 1, 1, 1e-3, g) == L.E_PROTOCOL  # plain submit inside a session
+    assert status_of(ctx.submit, 2, t0 + 2, 1, 1e-3, g) == L.E_STALE     # skipped part 1
+    assert status_of(ctx.submit, 1, t0 + 5, 1, 1e-3, g) == L.E_STALE     # step != t0 + part
+    assert status_of(ctx.submit, 1, t0 + 1, 0, 1e-3, g) == L.E_INVALID   # adam_t = 0
+    ctx.submit(1, t0 + 1, 1, 1e-3, g)
+    assert status_of(ctx.finalize) == L.E_PROTOCOL                      # before part K
+    for i in range(2, K + 1):
+        ctx.submit(i, t0 + i, i, 1e-3, g)
+    assert status_of(ctx.begin_checkpoint, t0 + K, K) == L.E_PROTOCOL   # unreleased checkpoint
+    ck = ctx.finalize()
+    assert ck.step == t0 + K - 1
+    assert status_of(ctx.begin_checkpoint, t0 + K, K) == L.E_PROTOCOL
+    ctx.release()
+    ctx.begin_checkpoint(t0 + K, 2)                                       # next session is fine
+    ctx.close()
+    # misaligned gradient
+    ctx2, _ = _make_ctx(G, state, K, part_align=8)
+    gbuf = torch.zeros(n + 8, dtype=torch.int16, device="cuda")
+    assert status_of(ctx2.submit, 0, 1, 1, 1e-3, gbuf[1:n + 1]) == L.E_INVALID
+    ctx2.close()
