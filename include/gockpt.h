@@ -149,7 +149,10 @@ typedef struct {
     double kernel_ms_total;        /* fused kernel time, timed steps */
     uint64_t kernel_launches_timed;
     double d2h_ms_total;           /* D2H stream busy time */
-    double last_session_stall_ms, last_session_d2h_ms, last_replay_ms, last_finalize_wait_ms;
+    double last_session_stall_ms, last_session_d2h_ms;
+    double last_replay_ms;         /* host replay compute time of the last session */
+    double last_worker_ms;         /* replay worker wall time: wait for the gradient log + replay + last drain */
+    double last_finalize_wait_ms;  /* time gck_finalize blocked */
     uint64_t last_session_d2h_bytes;
     uint64_t gpu_launches;         /* kernels this context launched */
     int32_t replay_threads;

@@ -71,7 +71,7 @@ class Stats(C.Structure):
                 ("d2h_bytes", C.c_uint64), ("stall_ms_total", C.c_double), ("stall_ms_max", C.c_double),
                 ("kernel_ms_total", C.c_double), ("kernel_launches_timed", C.c_uint64),
                 ("d2h_ms_total", C.c_double), ("last_session_stall_ms", C.c_double),
-                ("last_session_d2h_ms", C.c_double), ("last_replay_ms", C.c_double),
+                ("last_session_d2h_ms", C.c_double), ("last_replay_ms", C.c_double), ("last_worker_ms", C.c_double),
                 ("last_finalize_wait_ms", C.c_double), ("last_session_d2h_bytes", C.c_uint64),
                 ("gpu_launches", C.c_uint64), ("replay_threads", C.c_int32), ("_pad", C.c_int32)]
 

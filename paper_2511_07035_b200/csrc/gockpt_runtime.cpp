@@ -153,7 +153,8 @@ struct gck_ctx {
     std::condition_variable cv;
     bool worker_started = false, worker_done = false;
     gck_status worker_status = GCK_OK;
-    double replay_ms = 0;
+    double replay_ms = 0;          // worker wall time: waits for the drains + replay
+    double replay_compute_ms = 0;  // the host replay itself
     int replay_threads_used = 0;
 
     // bias-correction power cache (left-to-right binary64 running products)
@@ -206,8 +207,11 @@ struct gck_ctx {
             if (st == GCK_OK && !replayed) {
                 const uint16_t *gl[GCK_K_LIMIT];
                 for (uint32_t i = 0; i < K; ++i) gl[i] = glog[i];
+                const auto r0 = std::chrono::steady_clock::now();
                 st = gck::replay_host_impl(recs, K, lo, hi, h_master, h_m, h_v, gl, cfg.replay_threads,
                                            &replay_threads_used);
+                replay_compute_ms =
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - r0).count();
                 replayed = (st == GCK_OK);
             }
             if (st == GCK_OK) {
@@ -245,7 +249,8 @@ struct gck_ctx {
         stats.d2h_ms_total += d2h_ms;
         stats.last_session_stall_ms = stall;
         stats.last_session_d2h_ms = d2h_ms;
-        stats.last_replay_ms = replay_ms;
+        stats.last_replay_ms = replay_compute_ms;
+        stats.last_worker_ms = replay_ms;
         stats.replay_threads = replay_threads_used;
     }
 };
@@ -537,6 +542,7 @@ gck_status gck_begin_checkpoint(gck_ctx *c, uint64_t t0, uint32_t K) {
     c->worker_started = c->worker_done = false;
     c->worker_status = GCK_OK;
     c->replay_ms = 0;
+    c->replay_compute_ms = 0;
     c->stats.last_session_d2h_bytes = 0;
     c->state = State::ACTIVE;
     return GCK_OK;
