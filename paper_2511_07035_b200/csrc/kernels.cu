@@ -15,6 +15,9 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdlib>
+
 #include "internal.h"
 
 namespace gck {
@@ -121,6 +124,185 @@ __global__ void __launch_bounds__(256) fused_adamw_pack_kernel(const FusedArgs a
             a.v[e] = v;
         }
         if (a.out) a.out[e] = (uint16_t)(pack_bf16x2(p, 0.f) & 0xFFFFu);
+    }
+}
+
+// ---- TMA-pipelined variant of a2 (the default for n >= kTmaMinElems) ----
+// Persistent CTAs (2 per SM). One producer warp streams tiles of p, m, v (fp32) and g (bf16)
+// into a kStages-deep shared-memory ring with 1-D bulk async copies (cp.async.bulk, SASS
+// UBLKCP) completing on mbarriers; 8 consumer warps compute from shared memory and store
+// p', m', v', bf16(p') (and, in a session, the pre-update slot copy) with 16-B STG. Bytes in
+// flight per SM no longer depend on registers: up to 2 x kStages x 28 KiB.
+constexpr int kTile = 2048;                        // elements per tile
+constexpr uint64_t kTmaMinElems = 1u << 18;
+constexpr int kConsumerWarps = 8;                  // 256 threads x 8 elements = kTile
+constexpr int kStageBytes = kTile * 14;            // p, m, v fp32 + g bf16
+constexpr int tma_smem(int stages) { return stages * kStageBytes + 2 * stages * 8; }
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "GCK_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra GCK_WAIT;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t bytes) {
+    asm volatile("fence.proxy.async.shared::cta;\n\t"
+                 "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                 "r"(smem_u32(src)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+__device__ __forceinline__ void process4(const FusedArgs &a, const Rec &r, bool skip, bool pack, uint64_t e,
+                                         float4 p4, float4 m4, float4 v4, uint2 g2) {
+    float p[4] = {p4.x, p4.y, p4.z, p4.w}, m[4] = {m4.x, m4.y, m4.z, m4.w}, v[4] = {v4.x, v4.y, v4.z, v4.w};
+    if (pack) {
+        if (e >= a.lo && e < a.hi) {  // part boundaries are multiples of A (a multiple of 8)
+            const uint64_t o = e - a.lo;
+            *reinterpret_cast<float4 *>(a.sp + o) = p4;
+            *reinterpret_cast<float4 *>(a.sm + o) = m4;
+            *reinterpret_cast<float4 *>(a.sv + o) = v4;
+        }
+        if (e < a.ghi) *reinterpret_cast<uint2 *>(a.sg + e) = g2;
+    }
+    if (!skip) {
+        const uint32_t gb[4] = {g2.x & 0xFFFFu, g2.x >> 16, g2.y & 0xFFFFu, g2.y >> 16};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) adamw_elem(p[k], m[k], v[k], gb[k], r);
+        *reinterpret_cast<float4 *>(a.p + e) = make_float4(p[0], p[1], p[2], p[3]);
+        *reinterpret_cast<float4 *>(a.m + e) = make_float4(m[0], m[1], m[2], m[3]);
+        *reinterpret_cast<float4 *>(a.v + e) = make_float4(v[0], v[1], v[2], v[3]);
+    }
+    if (a.out) *reinterpret_cast<uint2 *>(a.out + e) = make_uint2(pack_bf16x2(p[0], p[1]), pack_bf16x2(p[2], p[3]));
+}
+
+template <bool PACK, int kStages, int kMinBlocks>
+__global__ void __launch_bounds__((kConsumerWarps + 1) * 32, kMinBlocks)
+    fused_adamw_pack_tma_kernel(const FusedArgs a) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem + kStages * kStageBytes);
+    uint64_t *empty = full + kStages;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t n_tiles = a.n / kTile;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kConsumerWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == kConsumerWarps) {  // producer warp: one elected lane issues the bulk copies
+        if (lane == 0) {
+            uint32_t k = 0;
+            for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++k) {
+                const int s = k % kStages;
+                const uint32_t ph = (k / kStages) & 1u;
+                mbar_wait(&empty[s], ph ^ 1u);
+                mbar_expect_tx(&full[s], kStageBytes);
+                uint8_t *st = smem + s * kStageBytes;
+                const uint64_t base = tile * kTile;
+                bulk_g2s(st, a.p + base, kTile * 4, &full[s]);
+                bulk_g2s(st + kTile * 4, a.m + base, kTile * 4, &full[s]);
+                bulk_g2s(st + kTile * 8, a.v + base, kTile * 4, &full[s]);
+                bulk_g2s(st + kTile * 12, a.g + base, kTile * 2, &full[s]);
+            }
+        }
+        return;
+    }
+    const Rec r = to_rec(a.rec);
+    const bool skip = a.rec.skip != 0;
+    const int c = threadIdx.x;  // consumer thread 0..255: elements [4c, 4c+4) and [1024+4c, 1024+4c+4)
+    uint32_t k = 0;
+    for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++k) {
+        const int s = k % kStages;
+        const uint32_t ph = (k / kStages) & 1u;
+        mbar_wait(&full[s], ph);
+        const uint8_t *st = smem + s * kStageBytes;
+        const uint64_t base = tile * kTile;
+        if (PACK && c == 0) {
+            // pack with bulk async stores straight from the staged tile (async proxy, no registers):
+            // the pre-update p, m, v of the tile's overlap with [lo, hi) and g of its overlap with [0, ghi)
+            const uint64_t olo = base > a.lo ? base : a.lo;
+            const uint64_t ohi = (base + kTile) < a.hi ? (base + kTile) : a.hi;
+            const uint64_t ghi = (base + kTile) < a.ghi ? (base + kTile) : a.ghi;
+            bool issued = false;
+            if (olo < ohi) {
+                const uint32_t off = (uint32_t)(olo - base), bytes = (uint32_t)(ohi - olo) * 4;
+                bulk_s2g(a.sp + (olo - a.lo), st + off * 4, bytes);
+                bulk_s2g(a.sm + (olo - a.lo), st + kTile * 4 + off * 4, bytes);
+                bulk_s2g(a.sv + (olo - a.lo), st + kTile * 8 + off * 4, bytes);
+                issued = true;
+            }
+            if (base < ghi) {
+                bulk_s2g(a.sg + base, st + kTile * 12, (uint32_t)(ghi - base) * 2);
+                issued = true;
+            }
+            if (issued) bulk_commit();
+        }
+        const float4 *sp = reinterpret_cast<const float4 *>(st);
+        const float4 *sm = reinterpret_cast<const float4 *>(st + kTile * 4);
+        const float4 *sv = reinterpret_cast<const float4 *>(st + kTile * 8);
+        const uint2 *sg = reinterpret_cast<const uint2 *>(st + kTile * 12);
+        const float4 p0 = sp[c], p1 = sp[c + kTile / 8];
+        const float4 m0 = sm[c], m1 = sm[c + kTile / 8];
+        const float4 v0 = sv[c], v1 = sv[c + kTile / 8];
+        const uint2 g0 = sg[c], g1 = sg[c + kTile / 8];
+        if (PACK && c == 0) bulk_wait_read();  // the bulk stores have read the stage
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);  // the stage may be refilled while we compute
+        const uint64_t e0 = base + 4 * (uint64_t)c;
+        process4(a, r, skip, false, e0, p0, m0, v0, g0);
+        process4(a, r, skip, false, e0 + kTile / 2, p1, m1, v1, g1);
+    }
+    if (PACK && c == 0) bulk_wait_all();  // slot writes complete before the CTA retires
+    // ragged tail [n_tiles*kTile, n): block 0's consumers, plain loads
+    if (blockIdx.x == 0) {
+        for (uint64_t e = n_tiles * kTile + (uint64_t)c; e < a.n; e += kConsumerWarps * 32) {
+            float p = a.p[e], m = a.m[e], v = a.v[e];
+            const uint32_t g = a.g[e];
+            if (PACK) {
+                if (e >= a.lo && e < a.hi) {
+                    a.sp[e - a.lo] = p;
+                    a.sm[e - a.lo] = m;
+                    a.sv[e - a.lo] = v;
+                }
+                if (e < a.ghi) a.sg[e] = (uint16_t)g;
+            }
+            if (!skip) {
+                adamw_elem(p, m, v, g, r);
+                a.p[e] = p;
+                a.m[e] = m;
+                a.v[e] = v;
+            }
+            if (a.out) a.out[e] = (uint16_t)(pack_bf16x2(p, 0.f) & 0xFFFFu);
+        }
     }
 }
 
@@ -244,9 +426,60 @@ inline unsigned grid_for(uint64_t work_items, unsigned block, int num_sms, unsig
 
 }  // namespace
 
+template <int S, int B>
+int launch_tma(const FusedArgs &a, bool pack, cudaStream_t s, int num_sms) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(fused_adamw_pack_tma_kernel<true, S, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             tma_smem(S));
+        cudaFuncSetAttribute(fused_adamw_pack_tma_kernel<false, S, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             tma_smem(S));
+        attr_set = true;
+    }
+    const uint64_t tiles = a.n / kTile;
+    const uint64_t cap = (uint64_t)(num_sms > 0 ? num_sms : 148) * B;
+    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, cap));
+    const unsigned block = (kConsumerWarps + 1) * 32;
+    if (pack)
+        fused_adamw_pack_tma_kernel<true, S, B><<<grid, block, tma_smem(S), s>>>(a);
+    else
+        fused_adamw_pack_tma_kernel<false, S, B><<<grid, block, tma_smem(S), s>>>(a);
+    return (int)cudaGetLastError();
+}
+
+int fused_impl_default() {
+    static int impl = [] {
+        const char *e = getenv("GCK_FUSED_IMPL");  // experiments only: "simple" | "tma"
+        if (e && e[0] == 's') return 1;
+        if (e && e[0] == 't') return 2;
+        return 0;
+    }();
+    return impl;
+}
+
 int launch_fused(const FusedArgs &a, bool pack, void *stream, int num_sms) {
-    const unsigned grid = grid_for(a.n >> 3, 256, num_sms, 8);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const int impl = fused_impl_default();
+    const bool aligned = ((reinterpret_cast<uintptr_t>(a.p) | reinterpret_cast<uintptr_t>(a.m) |
+                           reinterpret_cast<uintptr_t>(a.v) | reinterpret_cast<uintptr_t>(a.g)) & 15u) == 0;
+    if (aligned && (impl == 2 || (impl == 0 && a.n >= kTmaMinElems))) {
+        static int cfg = [] {  // experiments only: GCK_TMA_CFG = "stages,blocks_per_sm"
+            const char *e = getenv("GCK_TMA_CFG");
+            if (!e) return 61;
+            return (e[0] - '0') * 10 + (e[2] - '0');
+        }();
+        switch (cfg) {
+            case 23: return launch_tma<2, 3>(a, pack, s, num_sms);
+            case 22: return launch_tma<2, 2>(a, pack, s, num_sms);
+            case 42: return launch_tma<4, 2>(a, pack, s, num_sms);
+            case 32: return launch_tma<3, 2>(a, pack, s, num_sms);
+            case 51: return launch_tma<5, 1>(a, pack, s, num_sms);
+            case 71: return launch_tma<7, 1>(a, pack, s, num_sms);
+            case 81: return launch_tma<8, 1>(a, pack, s, num_sms);
+            default: return launch_tma<6, 1>(a, pack, s, num_sms);
+        }
+    }
+    const unsigned grid = grid_for(a.n >> 3, 256, num_sms, 8);
     if (pack)
         fused_adamw_pack_kernel<true><<<grid, 256, 0, s>>>(a);
     else
