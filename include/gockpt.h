@@ -250,6 +250,13 @@ gck_status gck_replay_device(const gck_step_record *recs, uint32_t K, const uint
 gck_status gck_adamw_step(const gck_step_record *rec, uint64_t n, float *d_master, float *d_m, float *d_v,
                           const uint16_t *d_grad, uint16_t *d_param_bf16, void *stream);
 
+/* a3 without a session: copy `bytes` from device memory to pinned host memory on `stream` by
+ * the drain's own mechanisms — GCK_COPY_ENGINE (cudaMemcpyAsync, in chunk_bytes pieces if
+ * nonzero) or GCK_COPY_ZEROCOPY (zc_ctas CTAs of 16-B stores; dst must be mapped pinned memory,
+ * both 16-B aligned). Async. Used by the host-link bandwidth sweep (BASELINE config 5). */
+gck_status gck_d2h_copy(void *dst_host, const void *src_dev, uint64_t bytes, int32_t mode, uint64_t chunk_bytes,
+                        uint32_t zc_ctas, void *stream);
+
 /* ---- harness-only (NOT the method): seeded synthetic inputs ------------- */
 
 /* Fill d_out with the counter-hash generator of gockpt_inputs.py (DESIGN.md

@@ -107,6 +107,7 @@ SIGNATURES = {
     "gck_adamw_step": (C.c_int, [C.POINTER(StepRecord), C.c_uint64, P, P, P, P, P, P]),
     "gck_h_generate": (C.c_int, [C.c_int32, C.c_int32, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
                                  C.c_uint32, P, P]),
+    "gck_d2h_copy": (C.c_int, [P, P, C.c_uint64, C.c_int32, C.c_uint64, C.c_uint32, P]),
     "gck_device_count": (C.c_int32, []),
 }
 

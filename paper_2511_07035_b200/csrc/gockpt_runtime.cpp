@@ -548,37 +548,49 @@ gck_status gck_begin_checkpoint(gck_ctx *c, uint64_t t0, uint32_t K) {
     return GCK_OK;
 }
 
+// a3 proper: move up to 4 (src device -> dst host) sections on stream `s`, by copy engine
+// (cudaMemcpyAsync, optionally in chunk-byte pieces) or by the zero-copy kernel (16-B SM stores
+// into the mapped pinned destination, dst_dev = its device view). Returns launches issued or -1.
+static int drain_sections(int mode, const void *const *src, void *const *dst, void *const *dst_dev,
+                          const uint64_t *bytes, int count, uint64_t chunk_bytes, uint32_t ctas, cudaStream_t s) {
+    if (mode == GCK_COPY_ZEROCOPY) {
+        ZcArgs z;
+        std::memset(&z, 0, sizeof(z));
+        for (int k = 0; k < count; ++k) {
+            if (!bytes[k]) continue;
+            z.src[z.count] = src[k];
+            z.dst[z.count] = dst_dev[k];
+            z.bytes[z.count] = bytes[k];
+            z.count++;
+        }
+        if (!z.count) return 0;
+        return gck::launch_zerocopy_drain(z, (int)ctas, s) ? -1 : 1;
+    }
+    const uint64_t chunk = chunk_bytes ? chunk_bytes : ~0ull;
+    for (int k = 0; k < count; ++k) {
+        for (uint64_t o = 0; o < bytes[k]; o += chunk) {
+            const uint64_t len = std::min(chunk, bytes[k] - o);
+            if (cudaMemcpyAsync((char *)dst[k] + o, (const char *)src[k] + o, len, cudaMemcpyDeviceToHost, s) !=
+                cudaSuccess)
+                return -1;
+        }
+    }
+    return 0;
+}
+
 static gck_status enqueue_drain(gck_ctx *c, uint32_t i, const SlotLayout &L, char *slot) {
-    // a3: slot -> host ckpt arrays at offset lo_i, gradient -> glog[i]
-    cudaError_t e;
+    // slot -> host ckpt arrays at offset lo_i, gradient -> glog[i]
     const uint64_t lo = c->lo[i - 1], pe = c->hi[i - 1] - lo;
     const uint64_t ghi = (i < c->K) ? c->hi[i - 1] : 0;
     const void *src[4] = {slot, slot + L.off_m, slot + L.off_v, slot + L.off_g};
     void *dst[4] = {c->h_master + lo, c->h_m + lo, c->h_v + lo, c->glog[i - 1]};
+    void *dst_dev[4];
+    for (int k = 0; k < 4; ++k) dst_dev[k] = dst[k] ? c->arena_dev + ((char *)dst[k] - c->arena) : nullptr;
     const uint64_t bytes[4] = {pe * 4, pe * 4, pe * 4, ghi * 2};
-    if (c->cfg.copy_mode == GCK_COPY_ZEROCOPY) {
-        ZcArgs z;
-        std::memset(&z, 0, sizeof(z));
-        for (int k = 0; k < 4; ++k) {
-            if (!bytes[k]) continue;
-            z.src[z.count] = src[k];
-            z.dst[z.count] = c->arena_dev + ((char *)dst[k] - c->arena);
-            z.bytes[z.count] = bytes[k];
-            z.count++;
-        }
-        if (gck::launch_zerocopy_drain(z, (int)c->cfg.zc_ctas, c->d2h)) return GCK_E_ABORTED;
-        c->stats.gpu_launches++;
-    } else {
-        const uint64_t chunk = c->cfg.chunk_bytes ? c->cfg.chunk_bytes : ~0ull;
-        for (int k = 0; k < 4; ++k) {
-            for (uint64_t o = 0; o < bytes[k]; o += chunk) {
-                const uint64_t len = std::min(chunk, bytes[k] - o);
-                e = cudaMemcpyAsync((char *)dst[k] + o, (const char *)src[k] + o, len, cudaMemcpyDeviceToHost,
-                                    c->d2h);
-                if (e != cudaSuccess) return GCK_E_ABORTED;
-            }
-        }
-    }
+    const int r = drain_sections(c->cfg.copy_mode, src, dst, dst_dev, bytes, 4, c->cfg.chunk_bytes, c->cfg.zc_ctas,
+                                 c->d2h);
+    if (r < 0) return GCK_E_ABORTED;
+    c->stats.gpu_launches += (uint64_t)r;
     const uint64_t tot = bytes[0] + bytes[1] + bytes[2] + bytes[3];
     c->stats.d2h_bytes += tot;
     c->stats.last_session_d2h_bytes += tot;
@@ -815,6 +827,28 @@ gck_status gck_replay_gpu(gck_ctx *c, void *stream, float *d_master, float *d_m,
     c->stats.gpu_launches++;
     e = cudaStreamSynchronize(s);
     if (e != cudaSuccess) return c->cuda_fail(e, "replay_gpu");
+    return GCK_OK;
+}
+
+gck_status gck_d2h_copy(void *dst_host, const void *src_dev, uint64_t bytes, int32_t mode, uint64_t chunk_bytes,
+                        uint32_t zc_ctas, void *stream) {
+    if (!dst_host || !src_dev) return set_tls(GCK_E_INVALID, "null argument");
+    if (mode != GCK_COPY_ENGINE && mode != GCK_COPY_ZEROCOPY) return set_tls(GCK_E_INVALID, "bad mode");
+    void *dst_dev = dst_host;
+    if (mode == GCK_COPY_ZEROCOPY) {
+        if (!aligned16(dst_host) || !aligned16(src_dev))
+            return set_tls(GCK_E_INVALID, "zero-copy needs 16-byte aligned buffers");
+        if (cudaHostGetDevicePointer(&dst_dev, dst_host, 0) != cudaSuccess) {
+            cudaGetLastError();
+            return set_tls(GCK_E_INVALID, "zero-copy destination is not mapped pinned memory");
+        }
+    }
+    const void *src[1] = {src_dev};
+    void *dst[1] = {dst_host};
+    void *dd[1] = {dst_dev};
+    const uint64_t b[1] = {bytes};
+    if (drain_sections(mode, src, dst, dd, b, 1, chunk_bytes, zc_ctas, static_cast<cudaStream_t>(stream)) < 0)
+        return set_tls(GCK_E_CUDA, std::string("d2h copy: ") + cudaGetErrorString(cudaGetLastError()));
     return GCK_OK;
 }
 

@@ -103,6 +103,14 @@ def adamw_step(rec, d_master, d_m, d_v, d_grad, d_param_bf16=None, stream=None):
                                _dptr(d_grad), _dptr(d_param_bf16), _stream_ptr(stream)))
 
 
+def d2h_copy(dst_host, src_dev, nbytes=None, mode="ce", chunk_bytes=0, zc_ctas=0, stream=None):
+    """a3 without a session (gck_d2h_copy): device tensor -> pinned host tensor, async on stream."""
+    nb = nbytes if nbytes is not None else src_dev.numel() * src_dev.element_size()
+    check(lib().gck_d2h_copy(dst_host.data_ptr(), _dptr(src_dev), nb,
+                             {"ce": L.COPY_ENGINE, "zerocopy": L.COPY_ZEROCOPY}[mode], chunk_bytes, zc_ctas,
+                             _stream_ptr(stream)))
+
+
 GEN_MASTER, GEN_EXP_AVG, GEN_EXP_AVG_SQ, GEN_GRAD = 1, 2, 3, 4
 
 

@@ -260,3 +260,16 @@ def test_protocol_errors(G):
     gbuf = torch.zeros(n + 8, dtype=torch.int16, device="cuda")
     assert status_of(ctx2.submit, 0, 1, 1, 1e-3, gbuf[1:n + 1]) == L.E_INVALID
     ctx2.close()
+
+
+# ---------------------------------------------------------------- a3 without a session
+@pytest.mark.parametrize("nbytes", [16, 4096 + 16, (1 << 24) + 48])
+@pytest.mark.parametrize("mode,chunk,ctas", [("ce", 0, 0), ("ce", 1 << 20, 0), ("zerocopy", 0, 7), ("zerocopy", 0, 148)])
+def test_d2h_copy_byte_exact(G, nbytes, mode, chunk, ctas):
+    src = torch.empty((nbytes + 1) // 2, dtype=torch.int16, device="cuda")
+    G.h_generate(4, src, 99, 1, 0, 0, 0)
+    dst = torch.zeros(nbytes + 64, dtype=torch.uint8, pin_memory=True)
+    G.d2h_copy(dst, src, nbytes, mode, chunk, ctas)
+    torch.cuda.synchronize()
+    assert torch.equal(dst[:nbytes], src.view(torch.uint8)[:nbytes].cpu())
+    assert not dst[nbytes:].any()          # nothing written past the end
