@@ -38,8 +38,12 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "per-step checkpoint stall ms & train throughput w/ ckpt; D2H GB/s vs link peak"
-N_GPT2 = 124_439_808
-WORKLOAD = "GPT-2 small 124M mixed-precision AdamW state, K=8 partitions, 1 B200"
+WORKLOADS = {  # BASELINE.json configs
+    "gpt2-small": "GPT-2 small 124M mixed-precision AdamW state, K=8 partitions, 1 B200",
+    "llama2-7b": "Llama-2 7B ZeRO-1 optimizer shards across 8\u00d7B200, K=8, checkpoint every 100 steps",
+    "llama2-13b": "Llama-2 13B ZeRO-1 across 2/4/8 B200, K sweep 2\u201316 (stall vs consistency-replay cost)",
+}
+DEFAULT_TOKENS = {"gpt2-small": 16 * 1024, "llama2-7b": 2 * 4096, "llama2-13b": 2048}
 HP = dict(beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01)
 LR = 3e-4
 T_WARM = 100  # updates already done before the bench starts (bias-correction count offset)
@@ -53,15 +57,19 @@ def parse():
     ap.add_argument("--impl", default="gockpt", choices=["gockpt", "reference"])
     ap.add_argument("--interval", type=int, default=50)
     ap.add_argument("--K", type=int, default=8)
-    ap.add_argument("--n", type=int, default=N_GPT2, help="optimizer-shard elements per rank")
-    ap.add_argument("--tokens", type=int, default=16 * 1024, help="tokens per step per rank (16 x 1024)")
+    ap.add_argument("--model", default="gpt2-small", choices=list(WORKLOADS))
+    ap.add_argument("--shard-of", type=int, default=0,
+                    help="ZeRO-1 data-parallel degree the shard is cut for (0 = the launched world size); "
+                         "e.g. 8 on one GPU = one rank of an 8-GPU job")
+    ap.add_argument("--n", type=int, default=0, help="override the optimizer-shard elements per rank")
+    ap.add_argument("--tokens", type=int, default=0, help="tokens per step per rank (0 = model default)")
     ap.add_argument("--copy-mode", default="ce", choices=["ce", "zerocopy"])
     ap.add_argument("--ring-slots", type=int, default=2)
     ap.add_argument("--replay-threads", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample", type=int, default=1 << 22,
-                    help="elements of the oracle sample (cpu_baseline leg; --impl reference uses 1/4 of it)")
+    ap.add_argument("--cpu-sample", type=int, default=1 << 24,
+                    help="elements of the oracle sample (cpu_baseline leg, ~15 s; --impl reference uses 1/16)")
     return ap.parse_args()
 
 
@@ -116,11 +124,26 @@ def oracle_interval_seconds(n_sample: int, K: int, interval: int, seed: int = 42
     return dt, 1
 
 
+def resolve(args):
+    """Per-rank shard size and tokens from --model / --shard-of (ZeRO-1)."""
+    from paper_2511_07035_b200.harness import MODELS, zero1_shard
+    world, rank, _ = dist_env()
+    W = args.shard_of or world
+    N = MODELS[args.model][0]
+    if not args.n:
+        args.n = N if W == 1 else zero1_shard(N, W, min(rank, W - 1), 512)[1]
+    if not args.tokens:
+        args.tokens = DEFAULT_TOKENS[args.model]
+    args.W = W
+    args.workload = WORKLOADS[args.model]
+    return args
+
+
 def run_reference(args):
     world, rank, _ = dist_env()
     if world > 1 and rank != 0:
         return
-    n_s = min(args.cpu_sample // 4, args.n)
+    n_s = min(args.cpu_sample // 16, args.n)
     for _ in range(args.warmup):
         oracle_interval_seconds(min(n_s, 1 << 16), args.K, args.interval)
     times = []
@@ -136,8 +159,8 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_interval * 1e3, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "n_per_rank": args.n, "K": args.K, "interval": args.interval,
-                   "tokens_per_step": args.tokens},
+        "config": {"workload": args.workload, "n_per_rank": args.n, "K": args.K, "interval": args.interval,
+                   "tokens_per_step": args.tokens, "zero1_degree": args.W},
         "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle",
                          "sample": f"{n_s} of {args.n} elements per interval, time x{args.n / n_s:.1f}; "
                                    f"the oracle's AdamW + capture + replay only (no F/B)",
@@ -149,7 +172,7 @@ def run_reference(args):
 
 # ----------------------------------------------------------------------------- the GPU arm
 def main():
-    args = parse()
+    args = resolve(parse())
     if args.impl == "reference":
         return run_reference(args)
     assert args.warmup >= 3, "W >= 3 warm-up steps"
@@ -159,7 +182,7 @@ def main():
 
     import paper_2511_07035_b200 as G
     from paper_2511_07035_b200 import build as gbuild
-    from paper_2511_07035_b200.harness import ClockSampler, Gpt2GemmStandIn, max_over_ranks, all_ranks_ok
+    from paper_2511_07035_b200.harness import ClockSampler, TransformerGemmStandIn, max_over_ranks, all_ranks_ok
 
     world, rank, local = dist_env()
     if not torch.cuda.is_available():
@@ -185,7 +208,7 @@ def main():
     if world > 1:
         full_grad = torch.empty(n * world, dtype=torch.bfloat16, device=dev)
         full_param = torch.empty(n * world, dtype=torch.bfloat16, device=dev)
-    fb = Gpt2GemmStandIn(tokens=T, device=dev)
+    fb = TransformerGemmStandIn(args.model, tokens=T, device=dev)
     fb.capture()
     ctx = G.GoCkpt(master, exp_avg, exp_avg_sq, param, **HP, k_min=K, k_max=K, part_align=1024,
                    ring_slots=args.ring_slots, copy_mode=args.copy_mode, replay_threads=args.replay_threads,
@@ -351,11 +374,13 @@ def main():
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": WORKLOAD, "n_per_rank": n, "K": K, "interval": I, "tokens_per_step_per_rank": T,
-                   "fb_standin": "GPT-2 small fwd+bwd GEMM chain (cuBLAS bf16, CUDA graph)",
+        "config": {"workload": args.workload, "n_per_rank": n, "K": K, "interval": I, "tokens_per_step_per_rank": T,
+                   "zero1_degree": args.W,
+                   "fb_standin": f"{args.model} fwd+bwd GEMM chain (cuBLAS bf16, CUDA graph)",
                    "fb_tflop_per_step": fb.flops / 1e12, "copy_mode": args.copy_mode,
                    "ring_slots": args.ring_slots, "parallelism": f"zero1-dp{world}",
-                   "l2": "inputs larger than L2 (1.5 GB fp32 state + 0.25 GB gradient per step per rank)",
+                   "l2": f"inputs larger than L2 ({12 * n / 1e9:.2f} GB fp32 state + {2 * n / 1e9:.2f} GB gradient "
+                         f"per step per rank)",
                    "step": "one checkpoint interval (I training steps, one K-part session, finalize)"},
         "stall": {"wait_ms_per_session_step": stall_wait_ms / (args.steps * K),
                   "wait_ms_max": st1["stall_ms_max"],

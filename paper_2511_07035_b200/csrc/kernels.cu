@@ -16,6 +16,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "internal.h"
@@ -135,7 +136,6 @@ __global__ void __launch_bounds__(256) fused_adamw_pack_kernel(const FusedArgs a
 // flight per SM no longer depend on registers: up to 2 x kStages x 28 KiB.
 constexpr int kTile = 2048;                        // elements per tile
 constexpr uint64_t kTmaMinElems = 1u << 18;
-constexpr int kConsumerWarps = 8;                  // 256 threads x 8 elements = kTile
 constexpr int kStageBytes = kTile * 14;            // p, m, v fp32 + g bf16
 constexpr int tma_smem(int stages) { return stages * kStageBytes + 2 * stages * 8; }
 
@@ -202,9 +202,13 @@ __device__ __forceinline__ void process4(const FusedArgs &a, const Rec &r, bool 
     if (a.out) *reinterpret_cast<uint2 *>(a.out + e) = make_uint2(pack_bf16x2(p[0], p[1]), pack_bf16x2(p[2], p[3]));
 }
 
-template <bool PACK, int kStages, int kMinBlocks>
-__global__ void __launch_bounds__((kConsumerWarps + 1) * 32, kMinBlocks)
-    fused_adamw_pack_tma_kernel(const FusedArgs a) {
+template <bool PACK, int kStages, int kMinBlocks, int kCW>
+__global__ void __launch_bounds__((kCW + 1) * 32, kMinBlocks) fused_adamw_pack_tma_kernel(const FusedArgs a) {
+    // kCW consumer warps; each consumer thread owns kQ float4 groups of the tile:
+    // elements [4(c + q*kCW*32), +4) for q < kQ (coalesced 16-B accesses across the warp).
+    constexpr int kThreads = kCW * 32;
+    constexpr int kQ = kTile / 4 / kThreads;
+    static_assert(kQ * kThreads * 4 == kTile, "tile must split evenly");
     extern __shared__ __align__(128) uint8_t smem[];
     uint64_t *full = reinterpret_cast<uint64_t *>(smem + kStages * kStageBytes);
     uint64_t *empty = full + kStages;
@@ -213,12 +217,12 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, kMinBlocks)
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kConsumerWarps);
+            mbar_init(&empty[s], kCW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    if (warp == kConsumerWarps) {  // producer warp: one elected lane issues the bulk copies
+    if (warp == kCW) {  // producer warp: one elected lane issues the bulk copies
         if (lane == 0) {
             uint32_t k = 0;
             for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++k) {
@@ -238,7 +242,7 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, kMinBlocks)
     }
     const Rec r = to_rec(a.rec);
     const bool skip = a.rec.skip != 0;
-    const int c = threadIdx.x;  // consumer thread 0..255: elements [4c, 4c+4) and [1024+4c, 1024+4c+4)
+    const int c = threadIdx.x;
     uint32_t k = 0;
     for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++k) {
         const int s = k % kStages;
@@ -270,21 +274,41 @@ __global__ void __launch_bounds__((kConsumerWarps + 1) * 32, kMinBlocks)
         const float4 *sm = reinterpret_cast<const float4 *>(st + kTile * 4);
         const float4 *sv = reinterpret_cast<const float4 *>(st + kTile * 8);
         const uint2 *sg = reinterpret_cast<const uint2 *>(st + kTile * 12);
-        const float4 p0 = sp[c], p1 = sp[c + kTile / 8];
-        const float4 m0 = sm[c], m1 = sm[c + kTile / 8];
-        const float4 v0 = sv[c], v1 = sv[c + kTile / 8];
-        const uint2 g0 = sg[c], g1 = sg[c + kTile / 8];
+        float4 pq[kQ], mq[kQ], vq[kQ];
+        uint2 gq[kQ];
+#pragma unroll
+        for (int q = 0; q < kQ; ++q) {
+            pq[q] = sp[c + q * kThreads];
+            mq[q] = sm[c + q * kThreads];
+            vq[q] = sv[c + q * kThreads];
+            gq[q] = sg[c + q * kThreads];
+        }
         if (PACK && c == 0) bulk_wait_read();  // the bulk stores have read the stage
+        // Release the stage only once every lane's shared-memory loads have landed in registers:
+        // a dependent instruction on all loaded values makes the scoreboard wait for the LDS
+        // results, __syncwarp orders the lanes before lane 0's arrive, and the proxy fence orders
+        // these generic-proxy reads before the async-proxy (TMA) refill of the same bytes (WAR).
+        uint32_t dep = 0;
+#pragma unroll
+        for (int q = 0; q < kQ; ++q)
+            dep ^= __float_as_uint(pq[q].x) ^ __float_as_uint(pq[q].w) ^ __float_as_uint(mq[q].x) ^
+                   __float_as_uint(mq[q].w) ^ __float_as_uint(vq[q].x) ^ __float_as_uint(vq[q].w) ^ gq[q].x ^ gq[q].y ^
+                   __float_as_uint(pq[q].y) ^ __float_as_uint(pq[q].z) ^ __float_as_uint(mq[q].y) ^
+                   __float_as_uint(mq[q].z) ^ __float_as_uint(vq[q].y) ^ __float_as_uint(vq[q].z);
+        asm volatile("" : "+r"(dep));
         __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);  // the stage may be refilled while we compute
-        const uint64_t e0 = base + 4 * (uint64_t)c;
-        process4(a, r, skip, false, e0, p0, m0, v0, g0);
-        process4(a, r, skip, false, e0 + kTile / 2, p1, m1, v1, g1);
+        if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_arrive(&empty[s]);  // the stage may be refilled while we compute
+        }
+#pragma unroll
+        for (int q = 0; q < kQ; ++q)
+            process4(a, r, skip, false, base + 4 * (uint64_t)(c + q * kThreads), pq[q], mq[q], vq[q], gq[q]);
     }
     if (PACK && c == 0) bulk_wait_all();  // slot writes complete before the CTA retires
     // ragged tail [n_tiles*kTile, n): block 0's consumers, plain loads
     if (blockIdx.x == 0) {
-        for (uint64_t e = n_tiles * kTile + (uint64_t)c; e < a.n; e += kConsumerWarps * 32) {
+        for (uint64_t e = n_tiles * kTile + (uint64_t)c; e < a.n; e += kThreads) {
             float p = a.p[e], m = a.m[e], v = a.v[e];
             const uint32_t g = a.g[e];
             if (PACK) {
@@ -426,35 +450,34 @@ inline unsigned grid_for(uint64_t work_items, unsigned block, int num_sms, unsig
 
 }  // namespace
 
-template <int S, int B>
+template <int S, int B, int CW>
 int launch_tma(const FusedArgs &a, bool pack, cudaStream_t s, int num_sms) {
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(fused_adamw_pack_tma_kernel<true, S, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             tma_smem(S));
-        cudaFuncSetAttribute(fused_adamw_pack_tma_kernel<false, S, B>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             tma_smem(S));
+        cudaFuncSetAttribute(fused_adamw_pack_tma_kernel<true, S, B, CW>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(S));
+        cudaFuncSetAttribute(fused_adamw_pack_tma_kernel<false, S, B, CW>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(S));
         attr_set = true;
     }
     const uint64_t tiles = a.n / kTile;
     const uint64_t cap = (uint64_t)(num_sms > 0 ? num_sms : 148) * B;
     const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, cap));
-    const unsigned block = (kConsumerWarps + 1) * 32;
+    const unsigned block = (CW + 1) * 32;
     if (pack)
-        fused_adamw_pack_tma_kernel<true, S, B><<<grid, block, tma_smem(S), s>>>(a);
+        fused_adamw_pack_tma_kernel<true, S, B, CW><<<grid, block, tma_smem(S), s>>>(a);
     else
-        fused_adamw_pack_tma_kernel<false, S, B><<<grid, block, tma_smem(S), s>>>(a);
+        fused_adamw_pack_tma_kernel<false, S, B, CW><<<grid, block, tma_smem(S), s>>>(a);
     return (int)cudaGetLastError();
 }
 
+// Kernel-variant overrides for experiments and differential tests, read at every launch:
+// GCK_FUSED_IMPL = "simple" | "tma", GCK_TMA_CFG = "stages,blocks_per_sm,consumer_warps".
 int fused_impl_default() {
-    static int impl = [] {
-        const char *e = getenv("GCK_FUSED_IMPL");  // experiments only: "simple" | "tma"
-        if (e && e[0] == 's') return 1;
-        if (e && e[0] == 't') return 2;
-        return 0;
-    }();
-    return impl;
+    const char *e = getenv("GCK_FUSED_IMPL");
+    if (e && e[0] == 's') return 1;
+    if (e && e[0] == 't') return 2;
+    return 0;
 }
 
 int launch_fused(const FusedArgs &a, bool pack, void *stream, int num_sms) {
@@ -463,20 +486,22 @@ int launch_fused(const FusedArgs &a, bool pack, void *stream, int num_sms) {
     const bool aligned = ((reinterpret_cast<uintptr_t>(a.p) | reinterpret_cast<uintptr_t>(a.m) |
                            reinterpret_cast<uintptr_t>(a.v) | reinterpret_cast<uintptr_t>(a.g)) & 15u) == 0;
     if (aligned && (impl == 2 || (impl == 0 && a.n >= kTmaMinElems))) {
-        static int cfg = [] {  // experiments only: GCK_TMA_CFG = "stages,blocks_per_sm"
+        const int cfg = [] {
             const char *e = getenv("GCK_TMA_CFG");
-            if (!e) return 61;
-            return (e[0] - '0') * 10 + (e[2] - '0');
+            if (!e) return 6116;
+            int st = 0, b = 0, cw = 0;
+            if (sscanf(e, "%d,%d,%d", &st, &b, &cw) != 3) return 6116;
+            return st * 1000 + b * 100 + cw;
         }();
         switch (cfg) {
-            case 23: return launch_tma<2, 3>(a, pack, s, num_sms);
-            case 22: return launch_tma<2, 2>(a, pack, s, num_sms);
-            case 42: return launch_tma<4, 2>(a, pack, s, num_sms);
-            case 32: return launch_tma<3, 2>(a, pack, s, num_sms);
-            case 51: return launch_tma<5, 1>(a, pack, s, num_sms);
-            case 71: return launch_tma<7, 1>(a, pack, s, num_sms);
-            case 81: return launch_tma<8, 1>(a, pack, s, num_sms);
-            default: return launch_tma<6, 1>(a, pack, s, num_sms);
+            case 6108: return launch_tma<6, 1, 8>(a, pack, s, num_sms);
+            case 6116: return launch_tma<6, 1, 16>(a, pack, s, num_sms);
+            case 4116: return launch_tma<4, 1, 16>(a, pack, s, num_sms);
+            case 8116: return launch_tma<8, 1, 16>(a, pack, s, num_sms);
+            case 3208: return launch_tma<3, 2, 8>(a, pack, s, num_sms);
+            case 3216: return launch_tma<3, 2, 16>(a, pack, s, num_sms);
+            case 3108: return launch_tma<3, 1, 8>(a, pack, s, num_sms);
+            default: return launch_tma<6, 1, 16>(a, pack, s, num_sms);
         }
     }
     const unsigned grid = grid_for(a.n >> 3, 256, num_sms, 8);

@@ -1,13 +1,12 @@
 """Training harness around the GoCkpt hot path (NOT the method; used by bench.py).
 
-  Gpt2GemmStandIn  the forward/backward stand-in: every GEMM of a GPT-2 small
-                   training step (12 layers, d=768, 12 heads, seq 1024, vocab
-                   50257 padded to 50304 as GPT-2 trainers do so cuBLAS can use
-                   its aligned sm_100 kernels; fwd + dgrad + wgrad, attention as
-                   batched GEMMs) on
-                   fixed random bf16 operands, captured once in a CUDA graph.
-                   cuBLAS library GEMMs: they stand for the step the checkpoint
-                   overlaps, they are not part of the checkpoint path.
+  TransformerGemmStandIn  the forward/backward stand-in: every GEMM of a
+                   GPT-2 small / Llama-2 7B / 13B training step (fwd + dgrad +
+                   wgrad, attention as batched GEMMs; GPT-2's vocab padded to
+                   50304 as GPT-2 trainers do so cuBLAS can use its aligned
+                   sm_100 kernels) on fixed random bf16 operands, captured once
+                   in a CUDA graph. cuBLAS library GEMMs: they stand for the step
+                   the checkpoint overlaps, they are not part of the checkpoint path.
   ClockSampler     nvidia-smi clocks / throttle reasons during the timed region.
   dist helpers     ZeRO-1 plumbing: every rank derives the same session schedule
                    from the global step (no communication on the checkpoint
@@ -24,53 +23,72 @@ import tempfile
 import torch
 
 
-class Gpt2GemmStandIn:
-    def __init__(self, tokens: int = 16 * 1024, d: int = 768, layers: int = 12, heads: int = 12,
-                 seq: int = 1024, vocab: int = 50304, device="cuda", seed: int = 0):
+MODELS = {
+    # name: (params, d, layers, heads, ffn, vocab, gated-MLP, seq); vocab padded to a multiple of 64
+    "gpt2-small": (124_439_808, 768, 12, 12, 3072, 50304, False, 1024),
+    "llama2-7b": (6_738_415_616, 4096, 32, 32, 11008, 32000, True, 4096),
+    "llama2-13b": (13_015_864_320, 5120, 40, 40, 13824, 32000, True, 4096),
+}
+
+
+class TransformerGemmStandIn:
+    """Every GEMM of one decoder-only transformer training step (forward, dgrad, wgrad) on
+    fixed random bf16 operands, in a CUDA graph: the F/B the checkpoint overlaps (harness).
+
+    Shapes follow the named model (MODELS); attention score/value products are batched
+    GEMMs over heads. Layers share one set of operand buffers (same FLOPs and shapes,
+    1/layers of the memory). cuBLAS library GEMMs, not part of the checkpoint path.
+    """
+
+    def __init__(self, model: str = "gpt2-small", tokens: int = 16 * 1024, device="cuda", seed: int = 0,
+                 seq: int | None = None):
+        _, d, layers, heads, ffn, vocab, gated, mseq = MODELS[model]
+        seq = min(seq or mseq, tokens)
         g = torch.Generator(device=device)
         g.manual_seed(seed)
         bf = torch.bfloat16
         self.flops = 0
-        self.ops = []  # (kind, A, B, C, dA, dB)
-        T, B = tokens, tokens // seq
+        self.ops = []  # (kind, A, B, C, dA, dB, repeat)
+        T, B = tokens, max(1, tokens // seq)
+        self.model, self.tokens = model, tokens
 
         def rnd(*shape):
             return (torch.randn(*shape, generator=g, device=device, dtype=torch.float32) * 0.02).to(bf)
 
-        def gemm(M, K, N):
+        def gemm(M, K, N, rep):
             A, Bm = rnd(M, K), rnd(K, N)
             C = torch.empty(M, N, device=device, dtype=bf)
-            self.ops.append(("mm", A, Bm, C, torch.empty_like(A), torch.empty_like(Bm)))
-            self.flops += 3 * 2 * M * K * N
+            self.ops.append(("mm", A, Bm, C, torch.empty_like(A), torch.empty_like(Bm), rep))
+            self.flops += rep * 3 * 2 * M * K * N
 
-        def bgemm(Bt, M, K, N):
+        def bgemm(Bt, M, K, N, rep):
             A, Bm = rnd(Bt, M, K), rnd(Bt, K, N)
             C = torch.empty(Bt, M, N, device=device, dtype=bf)
-            self.ops.append(("bmm", A, Bm, C, torch.empty_like(A), torch.empty_like(Bm)))
-            self.flops += 3 * 2 * Bt * M * K * N
+            self.ops.append(("bmm", A, Bm, C, torch.empty_like(A), torch.empty_like(Bm), rep))
+            self.flops += rep * 3 * 2 * Bt * M * K * N
 
         hd = d // heads
-        for _ in range(layers):
-            gemm(T, d, 3 * d)                  # qkv
-            bgemm(B * heads, seq, hd, seq)     # q k^T
-            bgemm(B * heads, seq, seq, hd)     # p v
-            gemm(T, d, d)                      # attn out
-            gemm(T, d, 4 * d)                  # fc
-            gemm(T, 4 * d, d)                  # proj
-        gemm(T, d, vocab)                      # lm head
+        gemm(T, d, 3 * d, layers)                  # qkv
+        bgemm(B * heads, seq, hd, seq, layers)     # q k^T
+        bgemm(B * heads, seq, seq, hd, layers)     # p v
+        gemm(T, d, d, layers)                      # attn out
+        gemm(T, d, (2 if gated else 1) * ffn, layers)  # fc (gate+up when gated)
+        gemm(T, ffn, d, layers)                    # down / proj
+        gemm(T, d, vocab, 1)                       # lm head
         self.graph = None
-        self.tokens = tokens
 
     def _run(self):
-        for kind, A, Bm, C, dA, dB in self.ops:       # forward
-            (torch.mm if kind == "mm" else torch.bmm)(A, Bm, out=C)
-        for kind, A, Bm, C, dA, dB in reversed(self.ops):  # backward: dgrad + wgrad
-            if kind == "mm":
-                torch.mm(C, Bm.t(), out=dA)
-                torch.mm(A.t(), C, out=dB)
-            else:
-                torch.bmm(C, Bm.transpose(1, 2), out=dA)
-                torch.bmm(A.transpose(1, 2), C, out=dB)
+        for kind, A, Bm, C, dA, dB, rep in self.ops:               # forward
+            for _ in range(rep):
+                (torch.mm if kind == "mm" else torch.bmm)(A, Bm, out=C)
+        for kind, A, Bm, C, dA, dB, rep in reversed(self.ops):     # backward: dgrad + wgrad
+            for _ in range(rep):
+                if kind == "mm":
+                    torch.mm(C, Bm.t(), out=dA)
+                    torch.mm(A.t(), C, out=dB)
+                else:
+                    torch.bmm(C, Bm.transpose(1, 2), out=dA)
+                    torch.bmm(A.transpose(1, 2), C, out=dB)
 
     def capture(self):
         s = torch.cuda.Stream()
@@ -89,6 +107,10 @@ class Gpt2GemmStandIn:
             self._run()
         else:
             self.graph.replay()
+
+
+def Gpt2GemmStandIn(tokens: int = 16 * 1024, device="cuda", seed: int = 0):
+    return TransformerGemmStandIn("gpt2-small", tokens, device, seed)
 
 
 class ClockSampler:

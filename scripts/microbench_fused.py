@@ -27,11 +27,24 @@ ctx = G.GoCkpt(p, m, v, out, k_min=K, k_max=K, timing=True)
 step = 0
 
 
+GEMM = os.environ.get("GCK_MB_GEMM") == "1"   # run a GEMM burst before each launch (power-capped clocks)
+if GEMM:
+    A = torch.randn(8192, 8192, device=dev, dtype=torch.bfloat16)
+    B = torch.randn(8192, 8192, device=dev, dtype=torch.bfloat16)
+
+
+def burst():
+    if GEMM:
+        for _ in range(8):
+            torch.mm(A, B)
+
+
 def plain(reps):
     global step
     ts = []
     for _ in range(reps):
         step += 1
+        burst()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record()
         ctx.submit(0, step, 100 + step, 3e-4, g)
@@ -49,6 +62,7 @@ for _ in range(3):
     s0 = ctx.stats()
     for i in range(1, K + 1):
         step += 1
+        burst()
         ctx.submit(i, step, 100 + step, 3e-4, g)
     ctx.finalize()
     s1 = ctx.stats()
@@ -71,7 +85,8 @@ ctx.release()
 parts = G.plan_parts(n, K, 1024)
 sess_bytes = sum(12 * (hi - lo) + (2 * hi if i < K - 1 else 0) for i, (lo, hi) in enumerate(parts))
 mean = statistics.mean(t_plain)
-print(json.dumps({"impl": os.environ.get("GCK_FUSED_IMPL", "auto"), "cfg": os.environ.get("GCK_TMA_CFG", "32"),
+print(json.dumps({"impl": os.environ.get("GCK_FUSED_IMPL", "auto"), "cfg": os.environ.get("GCK_TMA_CFG", "default"),
+                  "gemm_burst": GEMM,
                   "plain_us_mean": mean * 1e3, "plain_us_min": min(t_plain) * 1e3,
                   "plain_gbs": 28 * n / (mean / 1e3) / 1e9, "plain_gbs_best": 28 * n / (min(t_plain) / 1e3) / 1e9,
                   "session_us_mean": statistics.mean(sessions) * 1e3,

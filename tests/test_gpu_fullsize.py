@@ -117,3 +117,44 @@ def test_llama2_7b_zero1_rank_shard_fullsize(G):
     traj, _ = oracle_windows(idx, t0, K, seed)
     assert_state_equal(tuple(x[idx.astype(np.int64)] for x in ckpt), traj[K - 1], "7B shard vs oracle (windows)")
     assert stats["d2h_bytes"] == oracle.session_bytes(parts)
+
+
+@pytest.mark.parametrize("cfg", ["default", "6,1,8", "3,2,16"])
+def test_tma_kernel_stress_vs_simple_kernel(G, cfg, monkeypatch):
+    """Differential stress at the bench size: the TMA-pipelined fused kernel (the default) against
+    the plain grid-stride kernel (itself bit-exact against the oracle in test_gpu_parity), 24 steps
+    plain + session, every element compared bitwise after every step. Catches shared-memory ring
+    races (a stage refilled before every lane has read it) that window sampling can miss."""
+    import subprocess
+    import sys
+    import os
+    env = dict(os.environ)
+    if cfg != "default":
+        env["GCK_TMA_CFG"] = cfg
+    code = r'''
+import os, sys, torch
+sys.path.insert(0, ".")
+import paper_2511_07035_b200 as G
+n = 124_439_808
+def mk():
+    p = torch.empty(n, dtype=torch.float32, device="cuda"); m = torch.empty_like(p); v = torch.empty_like(p)
+    G.h_generate(1, p, 5, 0, 0, 0); G.h_generate(2, m, 5); G.h_generate(3, v, 5)
+    return p, m, v, torch.empty(n, dtype=torch.int16, device="cuda")
+a, b = mk(), mk()
+g = torch.empty(n, dtype=torch.int16, device="cuda")
+for s in range(1, 25):
+    G.h_generate(4, g, 5, s, 0, 1, 4)
+    r = G.make_step_record(0.9, 0.999, 1e-8, 0.01, 100 + s, 3e-4)
+    os.environ.pop("GCK_FUSED_IMPL", None)
+    G.adamw_step(r, *a[:3], g, a[3])                       # default launcher (TMA at this size)
+    os.environ["GCK_FUSED_IMPL"] = "simple"
+    G.adamw_step(r, *b[:3], g, b[3])                       # reference: the plain grid-stride kernel
+    torch.cuda.synchronize()
+    for x, y in zip(a, b):
+        assert torch.equal(x.view(torch.int32) if x.dtype == torch.float32 else x,
+                           y.view(torch.int32) if y.dtype == torch.float32 else y), ("step", s)
+print("ok")
+'''
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=600,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
