@@ -23,7 +23,7 @@ BUILD = os.path.join(ROOT, "build")
 LIB = os.path.join(PKG, "libgockpt.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["kernels.cu", "gockpt_runtime.cpp", "replay_host.cpp", "internal.h"]
+SOURCES = ["kernels.cu", "gockpt_runtime.cpp", "replay_host.cpp", "internal.h", "adamw_math.cuh"]
 
 
 def _cuda_home() -> str:

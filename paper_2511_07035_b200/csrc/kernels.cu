@@ -2,7 +2,9 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo (no --use_fast_math: IEEE
 //   division/sqrt and denormals are part of the normative update, R6/R13).
 //
-//  fused_adamw_pack  a2: one pass over the shard per training step. Loads p, m, v (fp32)
+//  fused_adamw_pack  a2: one pass over the shard per training step (two forms: the TMA-pipelined
+//                    kernel, default for n >= 2^18, on the branch-free fast paths of
+//                    adamw_math.cuh; and a plain grid-stride kernel on the reference intrinsics). Loads p, m, v (fp32)
 //                    and g (bf16); in a session, stores the PRE-update p, m, v of part i
 //                    and the raw g bits of the prefix [0, hi_i) into the HBM staging slot
 //                    (§4.2.1); applies the normative AdamW; stores p', m', v' and
@@ -19,30 +21,11 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include "adamw_math.cuh"
 #include "internal.h"
 
 namespace gck {
 namespace {
-
-struct Rec {
-    float b1, c1, b2, c2, bc1, bc2, lr, eps, wd, gs;
-};
-
-__device__ __forceinline__ Rec to_rec(const gck_step_record &s) {
-    return Rec{s.b1, s.c1, s.b2, s.c2, s.bc1, s.bc2, s.lr, s.eps, s.wd, s.gs};
-}
-
-// The normative update; every op is a correctly rounded
-// binary32 op with no contraction (the _rn intrinsics are never fused into FMA).
-__device__ __forceinline__ void adamw_elem(float &p, float &m, float &v, uint32_t gbits, const Rec &r) {
-    const float g = __fmul_rn(__uint_as_float(gbits << 16), r.gs);
-    m = __fadd_rn(__fmul_rn(r.b1, m), __fmul_rn(r.c1, g));
-    v = __fadd_rn(__fmul_rn(r.b2, v), __fmul_rn(r.c2, __fmul_rn(g, g)));
-    const float mh = __fdiv_rn(m, r.bc1);
-    const float vh = __fdiv_rn(v, r.bc2);
-    const float u = __fdiv_rn(mh, __fadd_rn(__fsqrt_rn(vh), r.eps));
-    p = __fsub_rn(p, __fmul_rn(r.lr, __fadd_rn(u, __fmul_rn(r.wd, p))));
-}
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);  // cvt.rn.bf16x2.f32: RNE
@@ -179,7 +162,7 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-__device__ __forceinline__ void process4(const FusedArgs &a, const Rec &r, bool skip, bool pack, uint64_t e,
+__device__ __forceinline__ void process4(const FusedArgs &a, const RecF &r, bool skip, bool pack, uint64_t e,
                                          float4 p4, float4 m4, float4 v4, uint2 g2) {
     float p[4] = {p4.x, p4.y, p4.z, p4.w}, m[4] = {m4.x, m4.y, m4.z, m4.w}, v[4] = {v4.x, v4.y, v4.z, v4.w};
     if (pack) {
@@ -194,7 +177,7 @@ __device__ __forceinline__ void process4(const FusedArgs &a, const Rec &r, bool 
     if (!skip) {
         const uint32_t gb[4] = {g2.x & 0xFFFFu, g2.x >> 16, g2.y & 0xFFFFu, g2.y >> 16};
 #pragma unroll
-        for (int k = 0; k < 4; ++k) adamw_elem(p[k], m[k], v[k], gb[k], r);
+        for (int k = 0; k < 4; ++k) adamw_elem_fast(p[k], m[k], v[k], gb[k], r);
         *reinterpret_cast<float4 *>(a.p + e) = make_float4(p[0], p[1], p[2], p[3]);
         *reinterpret_cast<float4 *>(a.m + e) = make_float4(m[0], m[1], m[2], m[3]);
         *reinterpret_cast<float4 *>(a.v + e) = make_float4(v[0], v[1], v[2], v[3]);
@@ -240,7 +223,7 @@ __global__ void __launch_bounds__((kCW + 1) * 32, kMinBlocks) fused_adamw_pack_t
         }
         return;
     }
-    const Rec r = to_rec(a.rec);
+    const RecF r = to_recf(a.rec);
     const bool skip = a.rec.skip != 0;
     const int c = threadIdx.x;
     uint32_t k = 0;
@@ -320,7 +303,7 @@ __global__ void __launch_bounds__((kCW + 1) * 32, kMinBlocks) fused_adamw_pack_t
                 if (e < a.ghi) a.sg[e] = (uint16_t)g;
             }
             if (!skip) {
-                adamw_elem(p, m, v, g, r);
+                adamw_elem_fast(p, m, v, g, r);
                 a.p[e] = p;
                 a.m[e] = m;
                 a.v[e] = v;
@@ -347,10 +330,10 @@ __global__ void __launch_bounds__(256) replay_kernel(const ReplayArgs a) {
             Vec8 p = ld8(a.p + e), m = ld8(a.m + e), v = ld8(a.v + e);
             for (uint32_t i = j; i + 1 < a.K; ++i) {  // updates t0+j+1 .. t0+K-1 (1-based: j+1..K-1)
                 if (a.rec[i].skip) continue;
-                const Rec r = to_rec(a.rec[i]);
+                const RecF r = to_recf(a.rec[i]);
                 const uint4 gq = *reinterpret_cast<const uint4 *>(a.glog[i] + e);
 #pragma unroll
-                for (int k = 0; k < 8; ++k) adamw_elem(p.x[k], m.x[k], v.x[k], bf16_lane(gq, k), r);
+                for (int k = 0; k < 8; ++k) adamw_elem_fast(p.x[k], m.x[k], v.x[k], bf16_lane(gq, k), r);
             }
             st8(a.p + e, p);
             st8(a.m + e, m);
@@ -361,7 +344,7 @@ __global__ void __launch_bounds__(256) replay_kernel(const ReplayArgs a) {
                 float p = a.p[q], m = a.m[q], v = a.v[q];
                 for (uint32_t i = jq; i + 1 < a.K; ++i) {
                     if (a.rec[i].skip) continue;
-                    adamw_elem(p, m, v, a.glog[i][q], to_rec(a.rec[i]));
+                    adamw_elem_fast(p, m, v, a.glog[i][q], to_recf(a.rec[i]));
                 }
                 a.p[q] = p;
                 a.m[q] = m;
