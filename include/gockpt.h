@@ -60,7 +60,9 @@ typedef enum {
     GCK_E_INCOMPLETE = 6, /* a session slice never arrived; the checkpoint is discarded */
     GCK_E_ABORTED = 7,    /* the checkpoint path failed; training continues, the session is void */
     GCK_E_BUSY = 8,       /* gck_finalize_poll: the checkpoint is not consistent yet */
-    GCK_E_NODEVICE = 9    /* no CUDA device (the library never falls back to the CPU) */
+    GCK_E_NODEVICE = 9,   /* no CUDA device (the library never falls back to the CPU) */
+    GCK_E_IO = 10,        /* persistence: a file operation failed (errno text in gck_last_error) */
+    GCK_E_CORRUPT = 11    /* persistence: bad magic/version, header/table/data CRC mismatch, truncation */
 } gck_status;
 
 typedef struct gck_ctx gck_ctx;
@@ -256,6 +258,68 @@ gck_status gck_adamw_step(const gck_step_record *rec, uint64_t n, float *d_maste
  * both 16-B aligned). Async. Used by the host-link bandwidth sweep (BASELINE config 5). */
 gck_status gck_d2h_copy(void *dst_host, const void *src_dev, uint64_t bytes, int32_t mode, uint64_t chunk_bytes,
                         uint32_t zc_ctas, void *stream);
+
+/* ---- NEXT-1: persistence and restore (§4.3.2, §4.4.1, §4.4.3) -------- */
+
+#define GCK_FILE_MAGIC "GOCKPT\0\1"
+#define GCK_FILE_VERSION 1u
+
+/* On-disk header of one rank's checkpoint file (little-endian, the first 4096 bytes). The CRC
+ * table (3 x nblocks uint32 CRC-32/zlib of each block_bytes block of master, exp_avg,
+ * exp_avg_sq) starts at table_offset; sections start at section_offset[], 4096-aligned. */
+typedef struct {
+    char magic[8];               /* GCK_FILE_MAGIC */
+    uint32_t version, header_bytes;
+    uint64_t step;               /* T: the checkpoint is the state after update T */
+    uint64_t adam_t;             /* bias-correction count of S(T) (resume with adam_t + 1) */
+    uint64_t n;
+    uint32_t rank, world;        /* ZeRO-1 shard identity */
+    double beta1, beta2, eps, weight_decay;
+    uint64_t block_bytes, nblocks, table_offset;
+    uint64_t section_offset[3], section_bytes[3];
+    uint32_t table_crc;          /* CRC-32 of the table's 3*nblocks entries */
+    uint32_t header_crc;         /* CRC-32 of every header byte before this field */
+} gck_file_header;
+
+typedef struct {
+    uint64_t bytes;              /* file bytes */
+    double seconds;              /* wall time of the call (write: through fsync, rename, metadata, LATEST) */
+    double data_seconds;         /* write: until the data + header were written (before fsync) */
+    double gbs;                  /* 3 x 4n bytes / seconds / 1e9 */
+    int32_t threads, _pad;
+} gck_persist_stats;
+
+/* Write a checkpoint file with `threads` writer threads (0 = min(16, cores)): data to
+ * `<path>.tmp` (disjoint 64 MiB blocks, CRC per block), then CRC table + header, fsync, rename
+ * to `path`, then `<path>.meta.json` (step, adam_t, n, rank, world, bytes, user JSON
+ * `meta_json` or null) and `<dir>/LATEST.rank<r>` (atomic rename) — "saving this metadata
+ * marks the completion of the latest checkpoint". hdr supplies step, adam_t, n, rank,
+ * world and the hyperparameters; the layout fields are filled in. Host-only, blocking.
+ * Errors: INVALID, IO, ABORTED (fault injection GCK_FAULT_PERSIST=<blocks>). */
+gck_status gck_write_checkpoint(const char *path, const gck_file_header *hdr, const float *master, const float *m,
+                                const float *v, int32_t threads, const char *meta_json, gck_persist_stats *stats);
+
+/* Read and validate (magic, version, header CRC) a checkpoint file's header. Host-only. */
+gck_status gck_read_header(const char *path, gck_file_header *out);
+
+/* Read a checkpoint file into host arrays of n floats each, verifying every block CRC
+ * ("first read from the SSD into CPU memory"). Host-only, blocking.
+ * Errors: INVALID (n mismatch), IO, CORRUPT. */
+gck_status gck_load_checkpoint(const char *path, uint64_t n, float *master, float *m, float *v, int32_t threads,
+                               gck_file_header *out, gck_persist_stats *stats);
+
+/* Persist the finalized checkpoint (state READY) in the background on a library thread;
+ * gck_release (and gck_destroy) wait for it, so the next session cannot begin before the
+ * previous checkpoint is durable ("GoCkpt will wait for the last checkpoint"). */
+gck_status gck_persist_begin(gck_ctx *ctx, const char *path, uint32_t rank, uint32_t world, const char *meta_json);
+
+/* Wait for the background persist; returns its status and stats. */
+gck_status gck_persist_wait(gck_ctx *ctx, gck_persist_stats *out);
+
+/* Restore (no session live): load `path` into the pinned arena, upload master/m/v into the
+ * context's device tensors on `stream`, re-derive the bf16 working copy RNE(master), and
+ * synchronize ("then transferred to GPU memory ... resumed at the step after"). */
+gck_status gck_restore(gck_ctx *ctx, const char *path, void *stream, gck_file_header *out);
 
 /* ---- harness-only (NOT the method): seeded synthetic inputs ------------- */
 

@@ -18,9 +18,10 @@ LIB_PATH = os.path.join(_HERE, "libgockpt.so")
 ABI_VERSION = 1
 K_LIMIT = 64
 
-OK, E_INVALID, E_PROTOCOL, E_STALE, E_NOMEM, E_CUDA, E_INCOMPLETE, E_ABORTED, E_BUSY, E_NODEVICE = range(10)
+(OK, E_INVALID, E_PROTOCOL, E_STALE, E_NOMEM, E_CUDA, E_INCOMPLETE, E_ABORTED, E_BUSY, E_NODEVICE, E_IO,
+ E_CORRUPT) = range(12)
 STATUS_NAMES = ["GCK_OK", "GCK_E_INVALID", "GCK_E_PROTOCOL", "GCK_E_STALE", "GCK_E_NOMEM", "GCK_E_CUDA",
-                "GCK_E_INCOMPLETE", "GCK_E_ABORTED", "GCK_E_BUSY", "GCK_E_NODEVICE"]
+                "GCK_E_INCOMPLETE", "GCK_E_ABORTED", "GCK_E_BUSY", "GCK_E_NODEVICE", "GCK_E_IO", "GCK_E_CORRUPT"]
 COPY_ENGINE, COPY_ZEROCOPY = 0, 1
 REPLAY_HOST, REPLAY_GPU = 0, 1
 
@@ -79,6 +80,23 @@ class Stats(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_ if not k.startswith("_")}
 
 
+class FileHeader(C.Structure):
+    _fields_ = [("magic", C.c_char * 8), ("version", C.c_uint32), ("header_bytes", C.c_uint32),
+                ("step", C.c_uint64), ("adam_t", C.c_uint64), ("n", C.c_uint64), ("rank", C.c_uint32),
+                ("world", C.c_uint32), ("beta1", C.c_double), ("beta2", C.c_double), ("eps", C.c_double),
+                ("weight_decay", C.c_double), ("block_bytes", C.c_uint64), ("nblocks", C.c_uint64),
+                ("table_offset", C.c_uint64), ("section_offset", C.c_uint64 * 3), ("section_bytes", C.c_uint64 * 3),
+                ("table_crc", C.c_uint32), ("header_crc", C.c_uint32)]
+
+
+class PersistStats(C.Structure):
+    _fields_ = [("bytes", C.c_uint64), ("seconds", C.c_double), ("data_seconds", C.c_double), ("gbs", C.c_double),
+                ("threads", C.c_int32), ("_pad", C.c_int32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_ if not k.startswith("_")}
+
+
 P = C.c_void_p
 U64P = C.POINTER(C.c_uint64)
 
@@ -108,6 +126,14 @@ SIGNATURES = {
     "gck_h_generate": (C.c_int, [C.c_int32, C.c_int32, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
                                  C.c_uint32, P, P]),
     "gck_d2h_copy": (C.c_int, [P, P, C.c_uint64, C.c_int32, C.c_uint64, C.c_uint32, P]),
+    "gck_write_checkpoint": (C.c_int, [C.c_char_p, C.POINTER(FileHeader), P, P, P, C.c_int32, C.c_char_p,
+                                       C.POINTER(PersistStats)]),
+    "gck_read_header": (C.c_int, [C.c_char_p, C.POINTER(FileHeader)]),
+    "gck_load_checkpoint": (C.c_int, [C.c_char_p, C.c_uint64, P, P, P, C.c_int32, C.POINTER(FileHeader),
+                                      C.POINTER(PersistStats)]),
+    "gck_persist_begin": (C.c_int, [P, C.c_char_p, C.c_uint32, C.c_uint32, C.c_char_p]),
+    "gck_persist_wait": (C.c_int, [P, C.POINTER(PersistStats)]),
+    "gck_restore": (C.c_int, [P, C.c_char_p, P, C.POINTER(FileHeader)]),
     "gck_device_count": (C.c_int32, []),
 }
 

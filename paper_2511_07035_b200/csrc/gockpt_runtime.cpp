@@ -157,6 +157,17 @@ struct gck_ctx {
     double replay_compute_ms = 0;  // the host replay itself
     int replay_threads_used = 0;
 
+    // bias-correction count tracking (the checkpoint records the count of S(T))
+    uint64_t count_known = 0;   // count after the last submitted update (0 until known)
+    uint64_t ckpt_adam_t = 0;
+
+    // background persist (NEXT-1)
+    std::thread persist_worker;
+    gck_status persist_status = GCK_OK;
+    gck_persist_stats persist_stats{};
+    std::string persist_error;
+    bool persist_started = false;
+
     // bias-correction power cache (left-to-right binary64 running products)
     uint64_t pow_t = 0;
     double pow1 = 1.0, pow2 = 1.0;
@@ -192,6 +203,9 @@ struct gck_ctx {
 
     void join_worker() {
         if (worker.joinable()) worker.join();
+    }
+    void join_persist() {
+        if (persist_worker.joinable()) persist_worker.join();
     }
 
     // Runs on the worker thread (eager) or inside finalize.
@@ -495,6 +509,7 @@ gck_status gck_create(const gck_config *cfg_in, const gck_hparams *hp, const gck
 gck_status gck_destroy(gck_ctx *c) {
     if (!c) return GCK_OK;
     c->join_worker();
+    c->join_persist();
     {
         DeviceGuard g(c->cfg.device);
         if (c->d2h) cudaStreamSynchronize(c->d2h);
@@ -615,6 +630,8 @@ gck_status gck_submit(gck_ctx *c, uint32_t part, const gck_step_args *a, void *s
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     gck_step_record rec;
     c->record_for(a->adam_t, a->lr, a->grad_scale, a->skip, &rec);
+    const uint64_t count_before = a->skip ? c->count_known : a->adam_t - 1;
+    c->count_known = a->skip ? c->count_known : a->adam_t;
 
     FusedArgs f;
     std::memset(&f, 0, sizeof(f));
@@ -635,6 +652,7 @@ gck_status gck_submit(gck_ctx *c, uint32_t part, const gck_step_args *a, void *s
     }
 
     const uint32_t i = part, slot_idx = (i - 1) % c->R;
+    if (i == c->K) c->ckpt_adam_t = count_before;  // S(t0+K-1) = the state this last update starts from
     const uint64_t lo = c->lo[i - 1], hi = c->hi[i - 1];
     const uint64_t ghi = (i < c->K) ? hi : 0;
     const SlotLayout L = slot_layout(hi - lo, ghi);
@@ -778,6 +796,7 @@ gck_status gck_release(gck_ctx *c) {
     if (c->state != State::READY && c->state != State::ABORTED)
         return c->fail(GCK_E_PROTOCOL, "release without a finalized checkpoint");
     c->join_worker();
+    c->join_persist();  // the next session may not begin before this checkpoint is durable
     c->state = State::IDLE;
     return GCK_OK;
 }
@@ -849,6 +868,101 @@ gck_status gck_d2h_copy(void *dst_host, const void *src_dev, uint64_t bytes, int
     const uint64_t b[1] = {bytes};
     if (drain_sections(mode, src, dst, dd, b, 1, chunk_bytes, zc_ctas, static_cast<cudaStream_t>(stream)) < 0)
         return set_tls(GCK_E_CUDA, std::string("d2h copy: ") + cudaGetErrorString(cudaGetLastError()));
+    return GCK_OK;
+}
+
+gck_status gck_write_checkpoint(const char *path, const gck_file_header *hdr, const float *master, const float *m,
+                                const float *v, int32_t threads, const char *meta_json, gck_persist_stats *stats) {
+    if (!path || !hdr || !master || !m || !v) return set_tls(GCK_E_INVALID, "null argument");
+    if (hdr->n == 0) return set_tls(GCK_E_INVALID, "n must be >= 1");
+    const float *sec[3] = {master, m, v};
+    std::string err;
+    const gck_status st = gck::write_checkpoint_impl(path, hdr, sec, threads, meta_json, stats, &err);
+    return st == GCK_OK ? st : set_tls(st, err);
+}
+
+gck_status gck_read_header(const char *path, gck_file_header *out) {
+    if (!path || !out) return set_tls(GCK_E_INVALID, "null argument");
+    std::string err;
+    const gck_status st = gck::read_header_impl(path, out, &err);
+    return st == GCK_OK ? st : set_tls(st, err);
+}
+
+gck_status gck_load_checkpoint(const char *path, uint64_t n, float *master, float *m, float *v, int32_t threads,
+                               gck_file_header *out, gck_persist_stats *stats) {
+    if (!path || !master || !m || !v || n == 0) return set_tls(GCK_E_INVALID, "null argument or n = 0");
+    float *dst[3] = {master, m, v};
+    std::string err;
+    const gck_status st = gck::load_checkpoint_impl(path, dst, n, threads, out, stats, &err);
+    return st == GCK_OK ? st : set_tls(st, err);
+}
+
+gck_status gck_persist_begin(gck_ctx *c, const char *path, uint32_t rank, uint32_t world, const char *meta_json) {
+    if (!c || !path) return set_tls(GCK_E_INVALID, "null argument");
+    if (c->state != State::READY) return c->fail(GCK_E_PROTOCOL, "persist needs a finalized, unreleased checkpoint");
+    if (c->persist_worker.joinable()) return c->fail(GCK_E_BUSY, "a persist is already running");
+    gck_file_header h;
+    std::memset(&h, 0, sizeof(h));
+    h.step = c->t0 + c->K - 1;
+    h.adam_t = c->ckpt_adam_t;
+    h.n = c->cfg.n;
+    h.rank = rank;
+    h.world = world ? world : 1;
+    h.beta1 = c->hp.beta1;
+    h.beta2 = c->hp.beta2;
+    h.eps = c->hp.eps;
+    h.weight_decay = c->hp.weight_decay;
+    const std::string p(path), meta(meta_json ? meta_json : "");
+    c->persist_status = GCK_OK;
+    c->persist_error.clear();
+    c->persist_started = true;
+    c->persist_worker = std::thread([c, h, p, meta]() {
+        const float *sec[3] = {c->h_master, c->h_m, c->h_v};
+        std::string err;
+        gck_persist_stats ps{};
+        const gck_status st = gck::write_checkpoint_impl(p.c_str(), &h, sec, c->cfg.replay_threads, meta.c_str(),
+                                                         &ps, &err);
+        c->persist_stats = ps;
+        c->persist_status = st;
+        c->persist_error = err;
+    });
+    return GCK_OK;
+}
+
+gck_status gck_persist_wait(gck_ctx *c, gck_persist_stats *out) {
+    if (!c) return set_tls(GCK_E_INVALID, "null ctx");
+    if (!c->persist_started) return c->fail(GCK_E_PROTOCOL, "no persist was started");
+    c->join_persist();
+    if (out) *out = c->persist_stats;
+    if (c->persist_status != GCK_OK) return c->fail(c->persist_status, c->persist_error);
+    return GCK_OK;
+}
+
+gck_status gck_restore(gck_ctx *c, const char *path, void *stream, gck_file_header *out) {
+    if (!c || !path) return set_tls(GCK_E_INVALID, "null argument");
+    if (c->state != State::IDLE) return c->fail(GCK_E_PROTOCOL, "restore while a session or checkpoint is live");
+    c->join_persist();
+    float *dst[3] = {c->h_master, c->h_m, c->h_v};
+    std::string err;
+    gck_file_header h;
+    gck_status st = gck::load_checkpoint_impl(path, dst, c->cfg.n, c->cfg.replay_threads, &h, nullptr, &err);
+    if (st != GCK_OK) return c->fail(st, err);
+    DeviceGuard g(c->cfg.device);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    const uint64_t b = c->cfg.n * 4;
+    cudaError_t e;
+    if ((e = cudaMemcpyAsync(c->t.master, c->h_master, b, cudaMemcpyHostToDevice, s)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(c->t.exp_avg, c->h_m, b, cudaMemcpyHostToDevice, s)) != cudaSuccess ||
+        (e = cudaMemcpyAsync(c->t.exp_avg_sq, c->h_v, b, cudaMemcpyHostToDevice, s)) != cudaSuccess)
+        return c->cuda_fail(e, "restore upload");
+    if (c->t.param_bf16) {
+        if (gck::launch_cast_bf16(c->t.master, c->t.param_bf16, c->cfg.n, stream, c->num_sms))
+            return c->cuda_fail(cudaGetLastError(), "restore bf16 cast");
+        c->stats.gpu_launches++;
+    }
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return c->cuda_fail(e, "restore");
+    c->count_known = h.adam_t;
+    if (out) *out = h;
     return GCK_OK;
 }
 

@@ -4,6 +4,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <string>
 
 #include "gockpt.h"
 
@@ -46,6 +47,15 @@ int launch_replay(const ReplayArgs &a, void *stream, int num_sms);
 int launch_zerocopy_drain(const ZcArgs &a, int ctas, void *stream);
 int launch_generate(int kind, int mode, uint64_t seed, uint64_t step, uint64_t offset, uint64_t n,
                     uint32_t zero_per_256, void *out, void *stream, int num_sms);
+
+int launch_cast_bf16(const float *src, uint16_t *dst, uint64_t n, void *stream, int num_sms);
+
+// Persistence (persist.cpp).
+gck_status write_checkpoint_impl(const char *path, const gck_file_header *hdr, const float *const sec[3], int threads,
+                                 const char *meta_json, gck_persist_stats *stats, std::string *err);
+gck_status read_header_impl(const char *path, gck_file_header *out, std::string *err);
+gck_status load_checkpoint_impl(const char *path, float *const dst[3], uint64_t n, int threads, gck_file_header *hdr_out,
+                                gck_persist_stats *stats, std::string *err);
 
 // Host replay (replay_host.cpp).
 gck_status replay_host_impl(const gck_step_record *recs, uint32_t K, const uint64_t *lo, const uint64_t *hi,

@@ -424,6 +424,12 @@ __global__ void generate_kernel(int kind, int mode, uint64_t key, uint64_t offse
     }
 }
 
+__global__ void cast_bf16_kernel(const float *src, uint16_t *dst, uint64_t n) {
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride)
+        dst[i] = (uint16_t)(pack_bf16x2(src[i], 0.f) & 0xFFFFu);
+}
+
 inline unsigned grid_for(uint64_t work_items, unsigned block, int num_sms, unsigned per_sm) {
     const uint64_t need = (work_items + block - 1) / block;
     const uint64_t cap = (uint64_t)(num_sms > 0 ? num_sms : 148) * per_sm;
@@ -499,6 +505,12 @@ int launch_replay(const ReplayArgs &a, void *stream, int num_sms) {
     if (a.n_replay == 0) return 0;
     const unsigned grid = grid_for((a.n_replay + 7) >> 3, 256, num_sms, 8);
     replay_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
+    return (int)cudaGetLastError();
+}
+
+int launch_cast_bf16(const float *src, uint16_t *dst, uint64_t n, void *stream, int num_sms) {
+    if (n == 0) return 0;
+    cast_bf16_kernel<<<grid_for(n, 256, num_sms, 8), 256, 0, static_cast<cudaStream_t>(stream)>>>(src, dst, n);
     return (int)cudaGetLastError();
 }
 

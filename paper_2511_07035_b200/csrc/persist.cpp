@@ -1,0 +1,358 @@
+// NEXT-1: persistence and restore of a consistent checkpoint (PAPER §4.3.2, §4.4.1 P:359,
+// §4.4.3).
+//
+//  - "the data persistence module uses multiple threads in parallel to save the model
+//    parameters to disk in the background": T writer threads pwrite disjoint 64 MiB
+//    blocks of the three sections, each computing the block's CRC-32 (zlib polynomial).
+//  - "After the model tensors are persisted, a callback function is used to save the
+//    pre-prepared checkpoint metadata ... Saving this metadata marks the completion of the
+//    latest checkpoint": the data goes to `<path>.tmp`, then the CRC table and the
+//    header, fsync, rename to `<path>` (atomic), then `<path>.meta.json`, then the directory's
+//    `LATEST` pointer (write + fsync + rename). A crash at any point leaves either the previous
+//    LATEST or the new one, never a torn checkpoint.
+//  - "When loading a checkpoint, it is first read from the SSD into CPU memory and then
+//    transferred to GPU memory": gck_load_checkpoint reads and verifies every block CRC;
+//    the context's restore path uploads it and re-derives the bf16 working copy.
+//
+// File layout (little-endian; see gck_file_header in gockpt.h): [0, 4096) header; [4096, ...)
+// the per-block CRC table (3 sections x nblocks uint32, padded to 4096); then master, exp_avg,
+// exp_avg_sq, each 4096-byte aligned.
+#include <errno.h>
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
+#include <zlib.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstddef>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "internal.h"
+
+namespace gck {
+namespace {
+
+constexpr uint64_t kBlock = 64ull << 20;
+constexpr uint64_t kPage = 4096;
+inline uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+struct Layout {
+    uint64_t sec_bytes, nblocks, table_off, table_bytes, sec_off[3], file_bytes;
+};
+
+Layout layout_for(uint64_t n) {
+    Layout L;
+    L.sec_bytes = n * 4;
+    L.nblocks = (L.sec_bytes + kBlock - 1) / kBlock;
+    L.table_off = kPage;
+    L.table_bytes = align_up(3 * L.nblocks * 4, kPage);
+    uint64_t off = L.table_off + L.table_bytes;
+    for (int s = 0; s < 3; ++s) {
+        L.sec_off[s] = off;
+        off = align_up(off + L.sec_bytes, kPage);
+    }
+    L.file_bytes = off;
+    return L;
+}
+
+bool pwrite_all(int fd, const void *buf, uint64_t len, uint64_t off) {
+    const char *p = static_cast<const char *>(buf);
+    while (len) {
+        const ssize_t w = ::pwrite(fd, p, std::min<uint64_t>(len, 1ull << 30), (off_t)off);
+        if (w < 0) {
+            if (errno == EINTR) continue;
+            return false;
+        }
+        p += w;
+        off += (uint64_t)w;
+        len -= (uint64_t)w;
+    }
+    return true;
+}
+
+bool pread_all(int fd, void *buf, uint64_t len, uint64_t off) {
+    char *p = static_cast<char *>(buf);
+    while (len) {
+        const ssize_t r = ::pread(fd, p, std::min<uint64_t>(len, 1ull << 30), (off_t)off);
+        if (r < 0) {
+            if (errno == EINTR) continue;
+            return false;
+        }
+        if (r == 0) return false;  // truncated
+        p += r;
+        off += (uint64_t)r;
+        len -= (uint64_t)r;
+    }
+    return true;
+}
+
+uint32_t crc32_of(const void *p, uint64_t len) {
+    uLong c = crc32(0L, Z_NULL, 0);
+    const Bytef *b = static_cast<const Bytef *>(p);
+    while (len) {
+        const uInt chunk = (uInt)std::min<uint64_t>(len, 1u << 30);
+        c = crc32(c, b, chunk);
+        b += chunk;
+        len -= chunk;
+    }
+    return (uint32_t)c;
+}
+
+bool write_small_file_atomic(const std::string &path, const std::string &content) {
+    const std::string tmp = path + ".tmp";
+    const int fd = ::open(tmp.c_str(), O_CREAT | O_TRUNC | O_WRONLY, 0644);
+    if (fd < 0) return false;
+    bool ok = pwrite_all(fd, content.data(), content.size(), 0) && ::fsync(fd) == 0;
+    ok = (::close(fd) == 0) && ok;
+    return ok && ::rename(tmp.c_str(), path.c_str()) == 0;
+}
+
+std::string dir_of(const std::string &path) {
+    const size_t k = path.find_last_of('/');
+    return k == std::string::npos ? std::string(".") : path.substr(0, k);
+}
+std::string base_of(const std::string &path) {
+    const size_t k = path.find_last_of('/');
+    return k == std::string::npos ? path : path.substr(k + 1);
+}
+
+void fsync_dir(const std::string &dir) {
+    const int fd = ::open(dir.c_str(), O_RDONLY | O_DIRECTORY);
+    if (fd >= 0) {
+        ::fsync(fd);
+        ::close(fd);
+    }
+}
+
+// Fault injection for the atomicity tests: GCK_FAULT_PERSIST=<k> makes the writer stop (as if
+// the process died) before writing data block k, i.e. before the header/rename/metadata/LATEST.
+long fault_after_blocks() {
+    const char *e = getenv("GCK_FAULT_PERSIST");
+    return e ? strtol(e, nullptr, 10) : -1;
+}
+
+}  // namespace
+
+gck_status write_checkpoint_impl(const char *path, const gck_file_header *hdr_in, const float *const sec[3],
+                                 int threads, const char *meta_json, gck_persist_stats *stats, std::string *err) {
+    const auto t0 = std::chrono::steady_clock::now();
+    if (!path || !hdr_in || !sec[0] || !sec[1] || !sec[2]) {
+        *err = "null argument";
+        return GCK_E_INVALID;
+    }
+    const uint64_t n = hdr_in->n;
+    const Layout L = layout_for(n);
+    const std::string final_path(path), tmp = final_path + ".tmp";
+    const int fd = ::open(tmp.c_str(), O_CREAT | O_TRUNC | O_WRONLY, 0644);
+    if (fd < 0) {
+        *err = "open " + tmp + ": " + strerror(errno);
+        return GCK_E_IO;
+    }
+    if (::ftruncate(fd, (off_t)L.file_bytes) != 0) {
+        *err = std::string("ftruncate: ") + strerror(errno);
+        ::close(fd);
+        return GCK_E_IO;
+    }
+    std::vector<uint32_t> table(3 * L.nblocks, 0);
+    const uint64_t total = 3 * L.nblocks;
+    std::atomic<uint64_t> next{0}, done_blocks{0};
+    std::atomic<bool> failed{false};
+    const long fault = fault_after_blocks();
+    auto worker = [&]() {
+        for (;;) {
+            const uint64_t j = next.fetch_add(1);
+            if (j >= total || failed.load()) break;
+            if (fault >= 0 && (long)j >= fault) {  // the writer "dies" before block j
+                failed = true;
+                break;
+            }
+            const int s = (int)(j / L.nblocks);
+            const uint64_t b = j % L.nblocks;
+            const uint64_t off = b * kBlock, len = std::min(kBlock, L.sec_bytes - off);
+            const char *src = reinterpret_cast<const char *>(sec[s]) + off;
+            table[j] = crc32_of(src, len);
+            if (!pwrite_all(fd, src, len, L.sec_off[s] + off)) failed = true;
+            done_blocks++;
+        }
+    };
+    if (threads <= 0) threads = std::min(16, default_threads());
+    threads = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)threads, total));
+    std::vector<std::thread> pool;
+    for (int k = 1; k < threads; ++k) pool.emplace_back(worker);
+    worker();
+    for (auto &t : pool) t.join();
+    if (failed) {
+        ::close(fd);
+        *err = fault >= 0 ? "fault injected (GCK_FAULT_PERSIST)" : std::string("pwrite: ") + strerror(errno);
+        return fault >= 0 ? GCK_E_ABORTED : GCK_E_IO;
+    }
+    // CRC table, then the header (with its own CRC) — the last bytes of the data file
+    std::vector<char> tbl(L.table_bytes, 0);
+    std::memcpy(tbl.data(), table.data(), table.size() * 4);
+    gck_file_header h = *hdr_in;
+    std::memcpy(h.magic, GCK_FILE_MAGIC, 8);
+    h.version = GCK_FILE_VERSION;
+    h.header_bytes = (uint32_t)kPage;
+    h.block_bytes = kBlock;
+    h.nblocks = L.nblocks;
+    h.table_offset = L.table_off;
+    for (int s = 0; s < 3; ++s) {
+        h.section_offset[s] = L.sec_off[s];
+        h.section_bytes[s] = L.sec_bytes;
+    }
+    h.table_crc = crc32_of(tbl.data(), table.size() * 4);
+    h.header_crc = 0;
+    h.header_crc = crc32_of(&h, offsetof(gck_file_header, header_crc));
+    std::vector<char> page(kPage, 0);
+    std::memcpy(page.data(), &h, sizeof(h));
+    bool ok = pwrite_all(fd, tbl.data(), tbl.size(), L.table_off) && pwrite_all(fd, page.data(), kPage, 0);
+    const auto t_data = std::chrono::steady_clock::now();
+    ok = ok && ::fsync(fd) == 0;
+    ok = (::close(fd) == 0) && ok;
+    if (!ok) {
+        *err = std::string("write/fsync: ") + strerror(errno);
+        return GCK_E_IO;
+    }
+    if (::rename(tmp.c_str(), final_path.c_str()) != 0) {
+        *err = std::string("rename: ") + strerror(errno);
+        return GCK_E_IO;
+    }
+    const std::string dir = dir_of(final_path);
+    fsync_dir(dir);
+    // metadata callback, then the LATEST pointer: the checkpoint is complete from here on
+    char meta[1024];
+    snprintf(meta, sizeof(meta),
+             "{\"file\": \"%s\", \"step\": %llu, \"adam_t\": %llu, \"n\": %llu, \"rank\": %u, \"world\": %u, "
+             "\"bytes\": %llu, \"user\": %s}\n",
+             base_of(final_path).c_str(), (unsigned long long)h.step, (unsigned long long)h.adam_t,
+             (unsigned long long)n, h.rank, h.world, (unsigned long long)L.file_bytes,
+             meta_json && *meta_json ? meta_json : "null");
+    if (!write_small_file_atomic(final_path + ".meta.json", meta) ||
+        !write_small_file_atomic(dir + "/LATEST.rank" + std::to_string(h.rank), base_of(final_path) + "\n")) {
+        *err = std::string("metadata/LATEST: ") + strerror(errno);
+        return GCK_E_IO;
+    }
+    fsync_dir(dir);
+    const auto t1 = std::chrono::steady_clock::now();
+    if (stats) {
+        stats->bytes = L.file_bytes;
+        stats->threads = threads;
+        stats->seconds = std::chrono::duration<double>(t1 - t0).count();
+        stats->data_seconds = std::chrono::duration<double>(t_data - t0).count();
+        stats->gbs = (double)(3 * L.sec_bytes) / stats->seconds / 1e9;
+    }
+    return GCK_OK;
+}
+
+gck_status read_header_impl(const char *path, gck_file_header *out, std::string *err) {
+    const int fd = ::open(path, O_RDONLY);
+    if (fd < 0) {
+        *err = std::string("open: ") + strerror(errno);
+        return GCK_E_IO;
+    }
+    std::vector<char> page(kPage);
+    const bool ok = pread_all(fd, page.data(), kPage, 0);
+    ::close(fd);
+    if (!ok) {
+        *err = "file shorter than its header";
+        return GCK_E_CORRUPT;
+    }
+    gck_file_header h;
+    std::memcpy(&h, page.data(), sizeof(h));
+    if (std::memcmp(h.magic, GCK_FILE_MAGIC, 8) != 0 || h.version != GCK_FILE_VERSION) {
+        *err = "not a GoCkpt checkpoint file (magic/version)";
+        return GCK_E_CORRUPT;
+    }
+    if (crc32_of(&h, offsetof(gck_file_header, header_crc)) != h.header_crc) {
+        *err = "header CRC mismatch";
+        return GCK_E_CORRUPT;
+    }
+    *out = h;
+    return GCK_OK;
+}
+
+gck_status load_checkpoint_impl(const char *path, float *const dst[3], uint64_t n, int threads,
+                                gck_file_header *hdr_out, gck_persist_stats *stats, std::string *err) {
+    const auto t0 = std::chrono::steady_clock::now();
+    gck_file_header h;
+    gck_status st = read_header_impl(path, &h, err);
+    if (st != GCK_OK) return st;
+    if (h.n != n) {
+        *err = "checkpoint n " + std::to_string(h.n) + " != expected " + std::to_string(n);
+        return GCK_E_INVALID;
+    }
+    const Layout L = layout_for(n);
+    if (h.nblocks != L.nblocks || h.table_offset != L.table_off) {
+        *err = "layout fields inconsistent with n";
+        return GCK_E_CORRUPT;
+    }
+    const int fd = ::open(path, O_RDONLY);
+    if (fd < 0) {
+        *err = std::string("open: ") + strerror(errno);
+        return GCK_E_IO;
+    }
+    std::vector<uint32_t> table(3 * L.nblocks);
+    if (!pread_all(fd, table.data(), table.size() * 4, L.table_off) ||
+        crc32_of(table.data(), table.size() * 4) != h.table_crc) {
+        ::close(fd);
+        *err = "CRC table unreadable or corrupt";
+        return GCK_E_CORRUPT;
+    }
+    const uint64_t total = 3 * L.nblocks;
+    std::atomic<uint64_t> next{0};
+    std::atomic<int> bad{0};  // 1 = io, 2 = crc
+    std::atomic<uint64_t> bad_block{0};
+    auto worker = [&]() {
+        for (;;) {
+            const uint64_t j = next.fetch_add(1);
+            if (j >= total || bad.load()) break;
+            const int s = (int)(j / L.nblocks);
+            const uint64_t b = j % L.nblocks;
+            const uint64_t off = b * kBlock, len = std::min(kBlock, L.sec_bytes - off);
+            char *p = reinterpret_cast<char *>(dst[s]) + off;
+            if (!pread_all(fd, p, len, L.sec_off[s] + off)) {
+                bad = 1;
+                break;
+            }
+            if (crc32_of(p, len) != table[j]) {
+                bad_block = j;
+                bad = 2;
+                break;
+            }
+        }
+    };
+    if (threads <= 0) threads = std::min(16, default_threads());
+    threads = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)threads, total));
+    std::vector<std::thread> pool;
+    for (int k = 1; k < threads; ++k) pool.emplace_back(worker);
+    worker();
+    for (auto &t : pool) t.join();
+    ::close(fd);
+    if (bad == 1) {
+        *err = "truncated or unreadable data section";
+        return GCK_E_CORRUPT;
+    }
+    if (bad == 2) {
+        *err = "data CRC mismatch in block " + std::to_string(bad_block.load());
+        return GCK_E_CORRUPT;
+    }
+    if (hdr_out) *hdr_out = h;
+    if (stats) {
+        const auto t1 = std::chrono::steady_clock::now();
+        stats->bytes = L.file_bytes;
+        stats->threads = threads;
+        stats->seconds = std::chrono::duration<double>(t1 - t0).count();
+        stats->data_seconds = stats->seconds;
+        stats->gbs = (double)(3 * L.sec_bytes) / stats->seconds / 1e9;
+    }
+    return GCK_OK;
+}
+
+}  // namespace gck

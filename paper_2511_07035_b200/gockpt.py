@@ -111,6 +111,41 @@ def d2h_copy(dst_host, src_dev, nbytes=None, mode="ce", chunk_bytes=0, zc_ctas=0
                              _stream_ptr(stream)))
 
 
+def _hdr_dict(h: L.FileHeader) -> dict:
+    return {"step": h.step, "adam_t": h.adam_t, "n": h.n, "rank": h.rank, "world": h.world, "beta1": h.beta1,
+            "beta2": h.beta2, "eps": h.eps, "weight_decay": h.weight_decay, "nblocks": h.nblocks,
+            "block_bytes": h.block_bytes}
+
+
+def write_checkpoint(path: str, master: np.ndarray, m: np.ndarray, v: np.ndarray, *, step: int, adam_t: int,
+                     rank: int = 0, world: int = 1, beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01,
+                     threads: int = 0, meta_json: str | None = None) -> dict:
+    """NEXT-1 (gck_write_checkpoint): multithreaded, CRC-protected, atomically published file."""
+    h = L.FileHeader()
+    h.step, h.adam_t, h.n, h.rank, h.world = step, adam_t, len(master), rank, world
+    h.beta1, h.beta2, h.eps, h.weight_decay = beta1, beta2, eps, weight_decay
+    st = L.PersistStats()
+    check(lib().gck_write_checkpoint(path.encode(), C.byref(h), _host_ptr(master, np.float32), _host_ptr(m, np.float32),
+                                     _host_ptr(v, np.float32), threads, meta_json.encode() if meta_json else None,
+                                     C.byref(st)))
+    return st.as_dict()
+
+
+def read_header(path: str) -> dict:
+    h = L.FileHeader()
+    check(lib().gck_read_header(path.encode(), C.byref(h)))
+    return _hdr_dict(h)
+
+
+def load_checkpoint(path: str, n: int, threads: int = 0):
+    """NEXT-1 (gck_load_checkpoint) -> (master, m, v, header dict, stats dict); every block CRC verified."""
+    out = [np.empty(n, np.float32) for _ in range(3)]
+    h, st = L.FileHeader(), L.PersistStats()
+    check(lib().gck_load_checkpoint(path.encode(), n, *[o.ctypes.data for o in out], threads, C.byref(h),
+                                    C.byref(st)))
+    return out[0], out[1], out[2], _hdr_dict(h), st.as_dict()
+
+
 GEN_MASTER, GEN_EXP_AVG, GEN_EXP_AVG_SQ, GEN_GRAD = 1, 2, 3, 4
 
 
@@ -201,6 +236,21 @@ class GoCkpt:
     def replay_gpu(self, d_master, d_m, d_v, d_glog, stream=None):
         check(lib().gck_replay_gpu(self._ctx, _stream_ptr(stream), _dptr(d_master), _dptr(d_m), _dptr(d_v),
                                    _dptr(d_glog)), self._ctx)
+
+    # -- NEXT-1 persistence / restore
+    def persist_begin(self, path: str, rank: int = 0, world: int = 1, meta_json: str | None = None):
+        check(lib().gck_persist_begin(self._ctx, path.encode(), rank, world,
+                                      meta_json.encode() if meta_json else None), self._ctx)
+
+    def persist_wait(self) -> dict:
+        st = L.PersistStats()
+        check(lib().gck_persist_wait(self._ctx, C.byref(st)), self._ctx)
+        return st.as_dict()
+
+    def restore(self, path: str, stream=None) -> dict:
+        h = L.FileHeader()
+        check(lib().gck_restore(self._ctx, path.encode(), _stream_ptr(stream), C.byref(h)), self._ctx)
+        return _hdr_dict(h)
 
     def stats(self) -> dict:
         s = L.Stats()

@@ -205,3 +205,24 @@ def zero1_shard(n_total: int, world: int, rank: int, align: int = 1024):
     padded = (n_total + unit - 1) // unit * unit
     n_r = padded // world
     return rank * n_r, n_r, padded
+
+
+def commit_global(directory: str, step: int, local_ok: bool, files: list[str] | None = None) -> bool:
+    """Global checkpoint commit ("Rank 0 monitoring completion by other Ranks"): every rank
+    reports whether its shard's file is durable; rank 0 writes MANIFEST.json (atomic rename) only
+    if all did. Returns whether the global checkpoint is complete."""
+    import json
+    import torch.distributed as dist
+    ok = all_ranks_ok(local_ok)
+    world = dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
+    rank = dist.get_rank() if dist.is_available() and dist.is_initialized() else 0
+    if ok and rank == 0:
+        man = {"step": step, "world": world,
+               "files": files or [f"ckpt_{step}.rank{r}.bin" for r in range(world)]}
+        tmp = os.path.join(directory, "MANIFEST.json.tmp")
+        with open(tmp, "w") as fh:
+            json.dump(man, fh)
+            fh.flush()
+            os.fsync(fh.fileno())
+        os.replace(tmp, os.path.join(directory, "MANIFEST.json"))
+    return ok

@@ -273,3 +273,58 @@ def test_d2h_copy_byte_exact(G, nbytes, mode, chunk, ctas):
     torch.cuda.synchronize()
     assert torch.equal(dst[:nbytes], src.view(torch.uint8)[:nbytes].cpu())
     assert not dst[nbytes:].any()          # nothing written past the end
+
+
+# ---------------------------------------------------------------- NEXT-1: persist + crash + restore + resume
+def test_persist_restore_resume_equals_uninterrupted(G, tmp_path):
+    """SPEC S:506 recovery correctness: train, checkpoint (GoCkpt session), persist in the
+    background, keep training, 'crash', restore from LATEST into a fresh context, resume at T+1
+    with the same gradients -> bit-identical to the run that never crashed."""
+    from oracle import ckpt_file as OF
+    n, K, seed = 300_007, 4, 21
+    state = gi.warm_state(seed, n)
+    total = 20
+    grads = [gi.grad_bits(seed, s, n) for s in range(1, total + 1)]
+
+    def train(ctx, steps, begin_at=None):
+        for s in steps:
+            part = 0
+            if begin_at is not None and begin_at < s <= begin_at + K:
+                if s == begin_at + 1:
+                    ctx.begin_checkpoint(begin_at, K)
+                part = s - begin_at
+            ctx.submit(part, s, s, 1e-3, up_u16(grads[s - 1]))
+
+    # uninterrupted reference run
+    p, m, v = (up_f32(x) for x in state)
+    ref = G.GoCkpt(p, m, v, None, **HP, k_min=K, k_max=K, part_align=64)
+    train(ref, range(1, total + 1))
+    torch.cuda.synchronize()
+    want = (down_f32(p), down_f32(m), down_f32(v))
+    ref.close()
+    # run with a checkpoint over steps 6..9 (T = 8), persisted while training continues to 13
+    p, m, v = (up_f32(x) for x in state)
+    ctx = G.GoCkpt(p, m, v, None, **HP, k_min=K, k_max=K, part_align=64)
+    train(ctx, range(1, 10), begin_at=5)
+    ck = ctx.finalize()
+    assert ck.step == 8
+    path = str(tmp_path / "ckpt_8.rank0.bin")
+    ctx.persist_begin(path, 0, 1, '{"note": "test"}')
+    train(ctx, range(10, 14))
+    st = ctx.persist_wait()
+    assert st["bytes"] > 12 * n
+    ctx.release()
+    ctx.close()                                                   # the crash
+    hdr, *_ = OF.read(OF.latest(str(tmp_path)))                    # the independent reader agrees
+    assert hdr["step"] == 8 and hdr["adam_t"] == 8
+    # fresh process state: garbage tensors, restore, resume at T+1 = 9
+    p2, m2, v2 = (torch.full((n,), 7.0, device="cuda") for _ in range(3))
+    out = torch.zeros(n, dtype=torch.int16, device="cuda")
+    ctx2 = G.GoCkpt(p2, m2, v2, out, **HP, k_min=K, k_max=K, part_align=64)
+    h = ctx2.restore(OF.latest(str(tmp_path)))
+    assert h["step"] == 8
+    assert np.array_equal(down_u16(out), oracle.rne_bf16(down_f32(p2)))   # working copy re-derived
+    train(ctx2, range(h["step"] + 1, total + 1))
+    torch.cuda.synchronize()
+    assert_state_equal((down_f32(p2), down_f32(m2), down_f32(v2)), want, "resumed vs uninterrupted")
+    ctx2.close()

@@ -54,6 +54,11 @@ def _worker(rank, world, port, n_total, K, t0, result_dir):
         lrecs = [G.make_step_record(0.9, 0.999, 1e-8, 0.01, t0 + i, 1e-3) for i in range(1, K + 1)]
         G.replay_host(lrecs, parts, p, m, v, [np.ascontiguousarray(x) for x in glog], threads=2)
         np.save(os.path.join(result_dir, f"rank{rank}.npy"), np.stack([p, m, v]))
+        # NEXT-1 per-rank persistence + rank-0 global commit
+        from paper_2511_07035_b200.harness import commit_global
+        path = os.path.join(result_dir, f"ckpt_{t0 + K - 1}.rank{rank}.bin")
+        G.write_checkpoint(path, p, m, v, step=t0 + K - 1, adam_t=t0 + K - 1, rank=rank, world=world, threads=2)
+        assert commit_global(result_dir, t0 + K - 1, True)
         t = max_over_ranks(float(rank + 1))
         assert t == float(world)
         assert all_ranks_ok(True)
@@ -77,6 +82,13 @@ def test_two_ranks_shard_checkpoints_concatenate_to_global(tmp_path, n_total):
     want = oracle.trajectory(p0, m0, v0, grads, recs)[-1]
     for g, w in zip(got, want):
         assert np.array_equal(g.view(np.uint32), w.view(np.uint32))
+    # the global manifest names every rank's durable file; reading them back gives S(T) again
+    import json
+    from oracle import ckpt_file as OF
+    man = json.load(open(tmp_path / "MANIFEST.json"))
+    assert man["step"] == t0 + K - 1 and man["world"] == world
+    back = np.concatenate([np.stack(OF.read(str(tmp_path / f))[1:]) for f in man["files"]], axis=1)
+    assert np.array_equal(back.view(np.uint32), got.view(np.uint32))
 
 
 def test_zero1_shard_layout():
