@@ -75,6 +75,7 @@ typedef struct {
 
 enum { GCK_COPY_ENGINE = 0, GCK_COPY_ZEROCOPY = 1 };
 enum { GCK_REPLAY_HOST = 0, GCK_REPLAY_GPU = 1 };
+enum { GCK_STAGE_RING = 0, GCK_STAGE_DIRECT = 1 };
 
 typedef struct {
     uint32_t abi_version;   /* must be GCK_ABI_VERSION */
@@ -95,6 +96,12 @@ typedef struct {
     int32_t eager_replay;   /* 1: replay starts on a library thread as soon as the gradient log is
                                complete (overlaps training); 0: replay runs inside gck_finalize
                                (lets tests read the staged bytes first) */
+    int32_t staging;        /* GCK_STAGE_RING: the fused kernel packs part i + G[0:hi_i] into an HBM
+                               ring slot (no transfer deadline on the compute stream but slot reuse).
+                               GCK_STAGE_DIRECT (GoCkpt-O literal; NEXT-2): no ring — part
+                               i is copied from the live arrays while step t0+i's F/B runs (the update
+                               waits for it) and G(t0+i)[0:hi_i] from the caller's gradient buffer,
+                               which the caller must not overwrite before gck_grad_fence. */
 } gck_config;
 
 /* Caller-owned device tensors (PyTorch owns them; they must outlive the context). */
@@ -190,6 +197,12 @@ gck_status gck_begin_checkpoint(gck_ctx *ctx, uint64_t t0, uint32_t K);
  * Errors: INVALID, PROTOCOL, STALE, CUDA (kernel launch failure poisons ctx),
  * ABORTED (the checkpoint path failed earlier; the update still ran). */
 gck_status gck_submit(gck_ctx *ctx, uint32_t part, const gck_step_args *args, void *stream);
+
+/* Direct staging: make `stream` wait until the gradient slice of the latest session step has
+ * been copied out of the caller's gradient buffer. Call before the next backward overwrites
+ * that buffer ("do not overwrite the original gradient space ... until the next
+ * backpropagation"). No-op in ring mode or outside sessions. */
+gck_status gck_grad_fence(gck_ctx *ctx, void *stream);
 
 /* Wait until every slot of the session has drained. Does not replay. */
 gck_status gck_wait_drained(gck_ctx *ctx);

@@ -24,6 +24,7 @@ STATUS_NAMES = ["GCK_OK", "GCK_E_INVALID", "GCK_E_PROTOCOL", "GCK_E_STALE", "GCK
                 "GCK_E_INCOMPLETE", "GCK_E_ABORTED", "GCK_E_BUSY", "GCK_E_NODEVICE", "GCK_E_IO", "GCK_E_CORRUPT"]
 COPY_ENGINE, COPY_ZEROCOPY = 0, 1
 REPLAY_HOST, REPLAY_GPU = 0, 1
+STAGE_RING, STAGE_DIRECT = 0, 1
 
 
 class Hparams(C.Structure):
@@ -35,7 +36,7 @@ class Config(C.Structure):
                 ("k_min", C.c_uint32), ("k_max", C.c_uint32), ("part_align", C.c_uint32),
                 ("ring_slots", C.c_uint32), ("copy_mode", C.c_int32), ("chunk_bytes", C.c_uint64),
                 ("zc_ctas", C.c_uint32), ("replay_mode", C.c_int32), ("replay_threads", C.c_int32),
-                ("timing", C.c_int32), ("eager_replay", C.c_int32)]
+                ("timing", C.c_int32), ("eager_replay", C.c_int32), ("staging", C.c_int32)]
 
 
 class Tensors(C.Structure):
@@ -107,6 +108,7 @@ SIGNATURES = {
     "gck_begin_checkpoint": (C.c_int, [P, C.c_uint64, C.c_uint32]),
     "gck_submit": (C.c_int, [P, C.c_uint32, C.POINTER(StepArgs), P]),
     "gck_wait_drained": (C.c_int, [P]),
+    "gck_grad_fence": (C.c_int, [P, P]),
     "gck_get_staged": (C.c_int, [P, C.POINTER(Staged)]),
     "gck_finalize": (C.c_int, [P, C.POINTER(Checkpoint)]),
     "gck_finalize_poll": (C.c_int, [P, C.POINTER(Checkpoint)]),

@@ -132,6 +132,12 @@ struct gck_ctx {
     uint64_t glog_elems_cap = 0;  // capacity in bf16 elements (incl. per-slice padding)
 
     cudaStream_t d2h = nullptr;
+    // direct staging (GoCkpt-O literal, NEXT-2): no ring; state D2H straight from the live arrays
+    bool direct = false;
+    bool upd_recorded = false;      // ev_upd holds the last fused kernel's completion
+    bool grad_copy_recorded = false;
+    cudaEvent_t ev_upd{}, ev_grad_src{}, ev_grad_copied{};
+    cudaEvent_t ev_state_copied[GCK_K_LIMIT]{};
     cudaEvent_t packed[2]{}, slot_free[2]{};
     bool slot_used[2]{};
     cudaEvent_t done[GCK_K_LIMIT]{};  // step i's slot fully drained (never re-recorded within a session)
@@ -417,6 +423,7 @@ gck_status gck_create(const gck_config *cfg_in, const gck_hparams *hp, const gck
     if (cfg.part_align % 8) return set_tls(GCK_E_INVALID, "part_align must be a multiple of 8");
     if (cfg.k_max < cfg.k_min || cfg.k_max > GCK_K_LIMIT) return set_tls(GCK_E_INVALID, "need 1 <= k_min <= k_max <= 64");
     if (cfg.ring_slots > 2) return set_tls(GCK_E_INVALID, "ring_slots must be 1 or 2");
+    if (cfg.staging != GCK_STAGE_RING && cfg.staging != GCK_STAGE_DIRECT) return set_tls(GCK_E_INVALID, "bad staging");
     if (cfg.copy_mode != GCK_COPY_ENGINE && cfg.copy_mode != GCK_COPY_ZEROCOPY)
         return set_tls(GCK_E_INVALID, "bad copy_mode");
     if (cfg.replay_mode != GCK_REPLAY_HOST) return set_tls(GCK_E_INVALID, "replay_mode: only GCK_REPLAY_HOST at finalize (GPU replay: gck_replay_gpu)");
@@ -457,9 +464,10 @@ gck_status gck_create(const gck_config *cfg_in, const gck_hparams *hp, const gck
         }
         glog_max = std::max(glog_max, gsum);
     }
-    c->slot_bytes = slot_max;
+    c->direct = (cfg.staging == GCK_STAGE_DIRECT);
+    c->slot_bytes = c->direct ? 0 : slot_max;
     c->glog_elems_cap = glog_max;
-    cudaError_t e = cudaMalloc((void **)&c->ring, c->slot_bytes * c->R);
+    cudaError_t e = c->direct ? cudaSuccess : cudaMalloc((void **)&c->ring, c->slot_bytes * c->R);
     if (e != cudaSuccess) {
         cudaGetLastError();
         delete c;
@@ -490,8 +498,12 @@ gck_status gck_create(const gck_config *cfg_in, const gck_hparams *hp, const gck
         ok = cudaEventCreateWithFlags(&c->packed[s], cudaEventDisableTiming) == cudaSuccess &&
              cudaEventCreateWithFlags(&c->slot_free[s], cudaEventDisableTiming) == cudaSuccess;
     }
+    ok = ok && cudaEventCreateWithFlags(&c->ev_upd, cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&c->ev_grad_src, cudaEventDisableTiming) == cudaSuccess &&
+         cudaEventCreateWithFlags(&c->ev_grad_copied, cudaEventDisableTiming) == cudaSuccess;
     for (uint32_t i = 0; i < GCK_K_LIMIT && ok; ++i) {
-        ok = cudaEventCreateWithFlags(&c->done[i], cudaEventDisableTiming) == cudaSuccess;
+        ok = cudaEventCreateWithFlags(&c->done[i], cudaEventDisableTiming) == cudaSuccess &&
+             cudaEventCreateWithFlags(&c->ev_state_copied[i], cudaEventDisableTiming) == cudaSuccess;
         if (ok && cfg.timing)
             ok = cudaEventCreate(&c->ev_w0[i]) == cudaSuccess && cudaEventCreate(&c->ev_w1[i]) == cudaSuccess &&
                  cudaEventCreate(&c->ev_k1[i]) == cudaSuccess && cudaEventCreate(&c->ev_d0[i]) == cudaSuccess &&
@@ -518,15 +530,40 @@ gck_status gck_destroy(gck_ctx *c) {
             if (c->slot_free[s]) cudaEventDestroy(c->slot_free[s]);
         }
         for (uint32_t i = 0; i < GCK_K_LIMIT; ++i) {
-            for (cudaEvent_t ev : {c->done[i], c->ev_w0[i], c->ev_w1[i], c->ev_k1[i], c->ev_d0[i], c->ev_d1[i]})
+            for (cudaEvent_t ev : {c->done[i], c->ev_w0[i], c->ev_w1[i], c->ev_k1[i], c->ev_d0[i], c->ev_d1[i],
+                                   c->ev_state_copied[i]})
                 if (ev) cudaEventDestroy(ev);
         }
+        for (cudaEvent_t ev : {c->ev_upd, c->ev_grad_src, c->ev_grad_copied})
+            if (ev) cudaEventDestroy(ev);
         if (c->d2h) cudaStreamDestroy(c->d2h);
         if (c->ring) cudaFree(c->ring);
         if (c->arena) cudaFreeHost(c->arena);
     }
     delete c;
     return GCK_OK;
+}
+
+static int drain_sections(int mode, const void *const *src, void *const *dst, void *const *dst_dev,
+                          const uint64_t *bytes, int count, uint64_t chunk_bytes, uint32_t ctas, cudaStream_t s);
+
+// Direct staging: D2H of part i's state [lo_i, hi_i) straight from the live arrays on the
+// side stream (ordered by the caller after the update that produced S(t0+i-1)).
+static cudaError_t enqueue_state_copy(gck_ctx *c, uint32_t i) {
+    const uint64_t lo = c->lo[i - 1], pe = c->hi[i - 1] - lo;
+    const void *src[3] = {c->t.master + lo, c->t.exp_avg + lo, c->t.exp_avg_sq + lo};
+    void *dst[3] = {c->h_master + lo, c->h_m + lo, c->h_v + lo};
+    void *dd[3];
+    for (int k = 0; k < 3; ++k) dd[k] = c->arena_dev + ((char *)dst[k] - c->arena);
+    const uint64_t bytes[3] = {pe * 4, pe * 4, pe * 4};
+    if (c->cfg.timing) cudaEventRecord(c->ev_d0[i - 1], c->d2h);
+    const int r = drain_sections(c->cfg.copy_mode, src, dst, dd, bytes, 3, c->cfg.chunk_bytes, c->cfg.zc_ctas, c->d2h);
+    if (r < 0) return cudaErrorUnknown;
+    c->stats.gpu_launches += (uint64_t)r;
+    if (c->cfg.timing) cudaEventRecord(c->ev_d1[i - 1], c->d2h);
+    c->stats.d2h_bytes += 3 * pe * 4;
+    c->stats.last_session_d2h_bytes += 3 * pe * 4;
+    return cudaEventRecord(c->ev_state_copied[i - 1], c->d2h);
 }
 
 gck_status gck_begin_checkpoint(gck_ctx *c, uint64_t t0, uint32_t K) {
@@ -550,6 +587,14 @@ gck_status gck_begin_checkpoint(gck_ctx *c, uint64_t t0, uint32_t K) {
         off += align_up(ghi, 128);
     }
     if (off > c->glog_elems_cap) return c->fail(GCK_E_INVALID, "gradient log capacity exceeded");
+    c->stats.last_session_d2h_bytes = 0;
+    if (c->direct) {
+        // part 1 = S(t0): copy it once the last update has finished (it overlaps step t0+1's F/B)
+        DeviceGuard g(c->cfg.device);
+        cudaError_t e = c->upd_recorded ? cudaStreamWaitEvent(c->d2h, c->ev_upd, 0) : cudaDeviceSynchronize();
+        if (e == cudaSuccess) e = enqueue_state_copy(c, 1);
+        if (e != cudaSuccess) return c->cuda_fail(e, "direct: part 1 copy");
+    }
     c->t0 = t0;
     c->K = K;
     c->next_part = 1;
@@ -558,7 +603,6 @@ gck_status gck_begin_checkpoint(gck_ctx *c, uint64_t t0, uint32_t K) {
     c->worker_status = GCK_OK;
     c->replay_ms = 0;
     c->replay_compute_ms = 0;
-    c->stats.last_session_d2h_bytes = 0;
     c->state = State::ACTIVE;
     return GCK_OK;
 }
@@ -612,6 +656,86 @@ static gck_status enqueue_drain(gck_ctx *c, uint32_t i, const SlotLayout &L, cha
     return GCK_OK;
 }
 
+static void finish_session_step(gck_ctx *c, uint32_t i) {
+    c->next_part++;
+    if (i == c->K) {
+        c->state = State::DRAINING;
+        c->stats.sessions++;
+        if (c->cfg.eager_replay) {
+            c->worker_started = true;
+            c->worker = std::thread([c]() { c->run_replay(); });
+        }
+    }
+}
+
+// Direct staging (GoCkpt-O): the gradient slice G(t0+i)[0:hi_i] is copied from the
+// caller's gradient buffer as soon as the backward that produced it is done (deadline: the
+// caller's next write of that buffer, gated by gck_grad_fence); the update waits only for the
+// state copy of part i, issued right after update t0+i-1 so it overlaps step t0+i's F/B.
+static gck_status submit_direct(gck_ctx *c, uint32_t i, const gck_step_args *a, cudaStream_t s, FusedArgs &f,
+                                const gck_step_record &rec, uint64_t count_before) {
+    if (i == c->K) c->ckpt_adam_t = count_before;
+    cudaError_t e;
+    if (i < c->K) {
+        const uint64_t ghi = c->hi[i - 1];
+        if ((e = cudaEventRecord(c->ev_grad_src, s)) != cudaSuccess ||
+            (e = cudaStreamWaitEvent(c->d2h, c->ev_grad_src, 0)) != cudaSuccess) {
+            c->abort_session(e, "direct: gradient event");
+            return GCK_E_ABORTED;
+        }
+        const void *src[1] = {a->grad_bf16};
+        void *dst[1] = {c->glog[i - 1]};
+        void *dd[1] = {c->arena_dev + ((char *)c->glog[i - 1] - c->arena)};
+        const uint64_t bytes[1] = {ghi * 2};
+        const int r = drain_sections(c->cfg.copy_mode, src, dst, dd, bytes, 1, c->cfg.chunk_bytes, c->cfg.zc_ctas,
+                                     c->d2h);
+        if (r < 0 || cudaEventRecord(c->ev_grad_copied, c->d2h) != cudaSuccess) {
+            c->abort_session(cudaGetLastError(), "direct: gradient copy");
+            return GCK_E_ABORTED;
+        }
+        c->grad_copy_recorded = true;
+        c->stats.gpu_launches += (uint64_t)r;
+        c->stats.d2h_bytes += ghi * 2;
+        c->stats.last_session_d2h_bytes += ghi * 2;
+    }
+    // a4 (direct): the update may not overwrite part i before its state copy has been taken
+    if (c->cfg.timing) cudaEventRecord(c->ev_w0[i - 1], s);
+    const bool ck_ok = cudaStreamWaitEvent(s, c->ev_state_copied[i - 1], 0) == cudaSuccess;
+    if (c->cfg.timing) cudaEventRecord(c->ev_w1[i - 1], s);
+    int le = gck::launch_fused(f, false, s, c->num_sms);
+    if (le) return c->cuda_fail((cudaError_t)le, "fused kernel launch");
+    c->stats.gpu_launches++;
+    c->stats.session_steps++;
+    if (c->cfg.timing) cudaEventRecord(c->ev_k1[i - 1], s);
+    cudaEventRecord(c->ev_upd, s);
+    c->upd_recorded = true;
+    if (!ck_ok) {
+        c->abort_session(cudaGetLastError(), "direct: state wait");
+        return GCK_E_ABORTED;
+    }
+    c->recs[i - 1] = rec;
+    if (i < c->K) {  // part i+1 = S(t0+i): copy it while step t0+i+1's F/B runs
+        if ((e = cudaStreamWaitEvent(c->d2h, c->ev_upd, 0)) != cudaSuccess || (e = enqueue_state_copy(c, i + 1)) != cudaSuccess) {
+            c->abort_session(e, "direct: state copy");
+            return GCK_E_ABORTED;
+        }
+    }
+    if ((e = cudaEventRecord(c->done[i - 1], c->d2h)) != cudaSuccess) {
+        c->abort_session(e, "direct: drain event");
+        return GCK_E_ABORTED;
+    }
+    finish_session_step(c, i);
+    return GCK_OK;
+}
+
+gck_status gck_grad_fence(gck_ctx *c, void *stream) {
+    if (!c) return set_tls(GCK_E_INVALID, "null ctx");
+    if (!c->direct || !c->grad_copy_recorded) return GCK_OK;
+    DeviceGuard g(c->cfg.device);
+    const cudaError_t e = cudaStreamWaitEvent(static_cast<cudaStream_t>(stream), c->ev_grad_copied, 0);
+    return e == cudaSuccess ? GCK_OK : c->cuda_fail(e, "grad fence");
+}
+
 gck_status gck_submit(gck_ctx *c, uint32_t part, const gck_step_args *a, void *stream) {
     if (!c) return set_tls(GCK_E_INVALID, "null ctx");
     if (!a || !a->grad_bf16) return c->fail(GCK_E_INVALID, "null step args or gradient");
@@ -648,8 +772,13 @@ gck_status gck_submit(gck_ctx *c, uint32_t part, const gck_step_args *a, void *s
         int e = gck::launch_fused(f, false, s, c->num_sms);
         if (e) return c->cuda_fail((cudaError_t)e, "fused kernel launch");
         c->stats.gpu_launches++;
+        if (c->direct) {
+            cudaEventRecord(c->ev_upd, s);
+            c->upd_recorded = true;
+        }
         return GCK_OK;
     }
+    if (c->direct) return submit_direct(c, part, a, s, f, rec, count_before);
 
     const uint32_t i = part, slot_idx = (i - 1) % c->R;
     if (i == c->K) c->ckpt_adam_t = count_before;  // S(t0+K-1) = the state this last update starts from
@@ -704,15 +833,7 @@ gck_status gck_submit(gck_ctx *c, uint32_t part, const gck_step_args *a, void *s
         return GCK_E_ABORTED;
     }
     c->slot_used[slot_idx] = true;
-    c->next_part++;
-    if (i == c->K) {
-        c->state = State::DRAINING;
-        c->stats.sessions++;
-        if (c->cfg.eager_replay) {
-            c->worker_started = true;
-            c->worker = std::thread([c]() { c->run_replay(); });
-        }
-    }
+    finish_session_step(c, i);
     return GCK_OK;
 }
 

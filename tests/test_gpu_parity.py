@@ -328,3 +328,51 @@ def test_persist_restore_resume_equals_uninterrupted(G, tmp_path):
     torch.cuda.synchronize()
     assert_state_equal((down_f32(p2), down_f32(m2), down_f32(v2)), want, "resumed vs uninterrupted")
     ctx2.close()
+
+
+# ---------------------------------------------------------------- NEXT-2: direct staging (GoCkpt-O literal)
+@pytest.mark.parametrize("n,K,A,copy", [(1 << 20, 4, 1024, "ce"), (1_000_003, 8, 1024, "ce"),
+                                        (300_007, 3, 8, "zerocopy"), (1 << 20, 1, 1024, "ce")])
+def test_direct_staging_session(G, n, K, A, copy):
+    """No HBM ring: part i is copied from the live arrays during step t0+i's F/B, the gradient
+    prefix from ONE reused gradient buffer that the 'backward' overwrites right after
+    gck_grad_fence. Staged bytes, host replay, GPU replay and snapshot as in ring mode."""
+    t0, seed = 10, 5
+    state, grads, recs, sargs = session_inputs(seed, n, K, t0)
+    p, m, v = (up_f32(x) for x in state)
+    ctx = G.GoCkpt(p, m, v, None, **HP, k_min=1, k_max=max(K, 8), part_align=A, copy_mode=copy,
+                   eager_replay=False, staging="direct")
+    gbuf = torch.empty(n, dtype=torch.int16, device="cuda")
+    for s in range(1, 3):                                   # plain steps before the session
+        gbuf.copy_(up_u16(gi.grad_bits(seed, 1000 + s, n)))
+        ctx.submit(0, t0 - 3 + s, t0 - 3 + s, 1e-3, gbuf)
+    torch.cuda.synchronize()
+    state = (down_f32(p), down_f32(m), down_f32(v))       # S(t0) after those steps
+    ctx.begin_checkpoint(t0, K)
+    snap = None
+    for i in range(1, K + 1):
+        ctx.grad_fence()                                    # the next backward may overwrite gbuf
+        gbuf.copy_(up_u16(grads[i - 1]))
+        if i == K:
+            snap = ctx.sync_snapshot()
+        a = sargs[i - 1]
+        ctx.submit(i, a["step"], a["adam_t"], a["lr"], gbuf, a["grad_scale"], a["skip"])
+    ctx.grad_fence()
+    gbuf.fill_(0)                                          # scribble the gradient buffer afterwards
+    ctx.wait_drained()
+    parts = oracle.make_parts(n, K, A)
+    cap, glog, _ = oracle.capture_session(*state, grads, recs, parts)
+    st = ctx.staged()
+    assert_state_equal((st["master"], st["exp_avg"], st["exp_avg_sq"]), oracle.assemble(cap), "direct staged")
+    for i in range(K - 1):
+        assert np.array_equal(st["glog"][i], glog[i]), f"direct glog {i + 1}"
+    dP, dM, dV = (torch.empty(n, dtype=torch.float32, device="cuda") for _ in range(3))
+    dG = torch.empty(max(1, n * (K - 1) + 128 * K), dtype=torch.int16, device="cuda")
+    ctx.replay_gpu(dP, dM, dV, dG)
+    assert_state_equal((down_f32(dP), down_f32(dM), down_f32(dV)), snap, "direct gpu replay vs snapshot")
+    ck = ctx.finalize()
+    assert_state_equal((ck.master, ck.exp_avg, ck.exp_avg_sq), snap, "direct host replay vs snapshot")
+    assert_state_equal((ck.master, ck.exp_avg, ck.exp_avg_sq), oracle.replay(cap, glog, recs, parts), "direct vs O2")
+    assert ctx.stats()["d2h_bytes"] == oracle.session_bytes(parts)
+    ctx.release()
+    ctx.close()
