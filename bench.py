@@ -65,6 +65,8 @@ def parse():
     ap.add_argument("--tokens", type=int, default=0, help="tokens per step per rank (0 = model default)")
     ap.add_argument("--copy-mode", default="ce", choices=["ce", "zerocopy"])
     ap.add_argument("--ring-slots", type=int, default=2)
+    ap.add_argument("--staging", default="ring", choices=["ring", "direct"],
+                    help="ring: fused kernel packs into an HBM ring; direct: GoCkpt-O literal (no ring)")
     ap.add_argument("--replay-threads", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -212,7 +214,7 @@ def main():
     fb.capture()
     ctx = G.GoCkpt(master, exp_avg, exp_avg_sq, param, **HP, k_min=K, k_max=K, part_align=1024,
                    ring_slots=args.ring_slots, copy_mode=args.copy_mode, replay_threads=args.replay_threads,
-                   timing=True, eager_replay=True)
+                   timing=True, eager_replay=True, staging=args.staging)
     parts = G.plan_parts(n, K, 1024)
     session_bytes = sum(12 * (hi - lo) + (2 * hi if i < K - 1 else 0) for i, (lo, hi) in enumerate(parts))
     state = {"step": 0, "gen": 0}
@@ -242,6 +244,7 @@ def main():
             ev.record(stream)
             step_events.append(ev)
         fb()                                                           # F/B stand-in
+        ctx.grad_fence(stream)   # direct staging: the last gradient slice is out before we overwrite
         if h_grad is not None:
             # e2e: the reduced gradient shard arrives from pinned host memory
             grad.copy_(h_grad[s % len(h_grad)], non_blocking=True)
@@ -378,7 +381,7 @@ def main():
                    "zero1_degree": args.W,
                    "fb_standin": f"{args.model} fwd+bwd GEMM chain (cuBLAS bf16, CUDA graph)",
                    "fb_tflop_per_step": fb.flops / 1e12, "copy_mode": args.copy_mode,
-                   "ring_slots": args.ring_slots, "parallelism": f"zero1-dp{world}",
+                   "ring_slots": args.ring_slots, "staging": args.staging, "parallelism": f"zero1-dp{world}",
                    "l2": f"inputs larger than L2 ({12 * n / 1e9:.2f} GB fp32 state + {2 * n / 1e9:.2f} GB gradient "
                          f"per step per rank)",
                    "step": "one checkpoint interval (I training steps, one K-part session, finalize)"},

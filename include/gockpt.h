@@ -334,6 +334,24 @@ gck_status gck_persist_wait(gck_ctx *ctx, gck_persist_stats *out);
  * synchronize ("then transferred to GPU memory ... resumed at the step after"). */
 gck_status gck_restore(gck_ctx *ctx, const char *path, void *stream, gck_file_header *out);
 
+/* ---- NEXT-4: analytic model (§3.1; §4.2.3) and K selection ------ */
+
+/* P = T_ckpt/(N T_step) + p N T_step/2 + p T_load; times in seconds, p in 1/s. */
+double gck_model_waste_fraction(double t_ckpt, double interval_steps, double t_step, double p_fail, double t_load);
+/* N* = sqrt(2 T_ckpt / (p T_step^2)). */
+double gck_model_optimal_interval(double t_ckpt, double t_step, double p_fail);
+/* P* = sqrt(2 p T_ckpt) + p T_load; GPU-utilization overhead is P* / (P* + 1). */
+double gck_model_optimal_waste(double t_ckpt, double p_fail, double t_load);
+/* Stall of one checkpoint: Async-O (N-1) T_step; GoCkpt share*N(N-1)/2 T_step (P:320,
+ * share = 1/7 in the paper's formula, 1/6 for a 12-B state + 2-B gradient, R4). */
+double gck_model_stall_async_o(uint32_t N, double t_step);
+double gck_model_stall_gockpt(uint32_t N, double t_step, double grad_share);
+/* Smallest K in [1, k_max] whose largest per-step D2H V_max(K) (a1 plan with alignment A)
+ * takes at most budget x t_step at link_gbs GB/s (SURVEY §8(d) K_min). *k_out = 0 and
+ * GCK_E_INVALID if none does. v_max_bytes (nullable) receives V_max of the chosen K. */
+gck_status gck_recommend_k(uint64_t n, uint32_t part_align, double link_gbs, double t_step_s, double budget,
+                           uint32_t k_max, uint32_t *k_out, double *v_max_bytes);
+
 /* ---- harness-only (NOT the method): seeded synthetic inputs ------------- */
 
 /* Fill d_out with the counter-hash generator of gockpt_inputs.py (DESIGN.md

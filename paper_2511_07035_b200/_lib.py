@@ -136,6 +136,13 @@ SIGNATURES = {
     "gck_persist_begin": (C.c_int, [P, C.c_char_p, C.c_uint32, C.c_uint32, C.c_char_p]),
     "gck_persist_wait": (C.c_int, [P, C.POINTER(PersistStats)]),
     "gck_restore": (C.c_int, [P, C.c_char_p, P, C.POINTER(FileHeader)]),
+    "gck_model_waste_fraction": (C.c_double, [C.c_double] * 5),
+    "gck_model_optimal_interval": (C.c_double, [C.c_double] * 3),
+    "gck_model_optimal_waste": (C.c_double, [C.c_double] * 3),
+    "gck_model_stall_async_o": (C.c_double, [C.c_uint32, C.c_double]),
+    "gck_model_stall_gockpt": (C.c_double, [C.c_uint32, C.c_double, C.c_double]),
+    "gck_recommend_k": (C.c_int, [C.c_uint64, C.c_uint32, C.c_double, C.c_double, C.c_double, C.c_uint32,
+                                  C.POINTER(C.c_uint32), C.POINTER(C.c_double)]),
     "gck_device_count": (C.c_int32, []),
 }
 

@@ -23,7 +23,7 @@ BUILD = os.path.join(ROOT, "build")
 LIB = os.path.join(PKG, "libgockpt.so")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-SOURCES = ["kernels.cu", "gockpt_runtime.cpp", "replay_host.cpp", "persist.cpp", "internal.h", "adamw_math.cuh"]
+SOURCES = ["kernels.cu", "gockpt_runtime.cpp", "replay_host.cpp", "persist.cpp", "model.cpp", "internal.h", "adamw_math.cuh"]
 
 
 def _cuda_home() -> str:
@@ -61,7 +61,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     log: list[str] = []
     inc = ["-I", INCLUDE, "-I", CSRC]
-    objs = {k: os.path.join(BUILD, k + ".o") for k in ("kernels", "runtime", "replay_host", "persist")}
+    objs = {k: os.path.join(BUILD, k + ".o") for k in ("kernels", "runtime", "replay_host", "persist", "model")}
     _run([nvcc, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xptxas", "-v", "-Xcompiler", "-fPIC", *inc,
           "-c", os.path.join(CSRC, "kernels.cu"), "-o", objs["kernels"]], log)
     gxx = ["g++", "-O3", "-std=c++17", "-fPIC", "-Wall", "-Wno-unused-function", *inc,
@@ -70,9 +70,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
     _run(gxx + ["-ffp-contract=off", "-fno-math-errno",
                 "-c", os.path.join(CSRC, "replay_host.cpp"), "-o", objs["replay_host"]], log)
     _run(gxx + ["-c", os.path.join(CSRC, "persist.cpp"), "-o", objs["persist"]], log)
+    _run(gxx + ["-c", os.path.join(CSRC, "model.cpp"), "-o", objs["model"]], log)
     tmp = LIB + ".tmp"
     _run([nvcc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, objs["kernels"], objs["runtime"],
-          objs["replay_host"], objs["persist"], "-Xcompiler", "-fPIC", "-lpthread", "-lz"], log)
+          objs["replay_host"], objs["persist"], objs["model"], "-Xcompiler", "-fPIC", "-lpthread", "-lz"], log)
     os.replace(tmp, LIB)
     with open(os.path.join(BUILD, "build.log"), "w") as fh:
         fh.write("\n".join(log))

@@ -138,6 +138,7 @@ struct gck_ctx {
     bool grad_copy_recorded = false;
     cudaEvent_t ev_upd{}, ev_grad_src{}, ev_grad_copied{};
     cudaEvent_t ev_state_copied[GCK_K_LIMIT]{};
+    cudaEvent_t ev_g0[GCK_K_LIMIT]{}, ev_g1[GCK_K_LIMIT]{};  // direct: gradient-copy timing
     cudaEvent_t packed[2]{}, slot_free[2]{};
     bool slot_used[2]{};
     cudaEvent_t done[GCK_K_LIMIT]{};  // step i's slot fully drained (never re-recorded within a session)
@@ -262,6 +263,8 @@ struct gck_ctx {
                     stats.kernel_launches_timed++;
                 }
                 if (cudaEventElapsedTime(&c, ev_d0[i], ev_d1[i]) == cudaSuccess) d2h_ms += c;
+                float gms = 0;
+                if (direct && i + 1 < K && cudaEventElapsedTime(&gms, ev_g0[i], ev_g1[i]) == cudaSuccess) d2h_ms += gms;
             }
         }
         stats.stall_ms_total += stall;
@@ -505,7 +508,8 @@ gck_status gck_create(const gck_config *cfg_in, const gck_hparams *hp, const gck
         ok = cudaEventCreateWithFlags(&c->done[i], cudaEventDisableTiming) == cudaSuccess &&
              cudaEventCreateWithFlags(&c->ev_state_copied[i], cudaEventDisableTiming) == cudaSuccess;
         if (ok && cfg.timing)
-            ok = cudaEventCreate(&c->ev_w0[i]) == cudaSuccess && cudaEventCreate(&c->ev_w1[i]) == cudaSuccess &&
+            ok = cudaEventCreate(&c->ev_g0[i]) == cudaSuccess && cudaEventCreate(&c->ev_g1[i]) == cudaSuccess &&
+                 cudaEventCreate(&c->ev_w0[i]) == cudaSuccess && cudaEventCreate(&c->ev_w1[i]) == cudaSuccess &&
                  cudaEventCreate(&c->ev_k1[i]) == cudaSuccess && cudaEventCreate(&c->ev_d0[i]) == cudaSuccess &&
                  cudaEventCreate(&c->ev_d1[i]) == cudaSuccess;
     }
@@ -531,7 +535,7 @@ gck_status gck_destroy(gck_ctx *c) {
         }
         for (uint32_t i = 0; i < GCK_K_LIMIT; ++i) {
             for (cudaEvent_t ev : {c->done[i], c->ev_w0[i], c->ev_w1[i], c->ev_k1[i], c->ev_d0[i], c->ev_d1[i],
-                                   c->ev_state_copied[i]})
+                                   c->ev_state_copied[i], c->ev_g0[i], c->ev_g1[i]})
                 if (ev) cudaEventDestroy(ev);
         }
         for (cudaEvent_t ev : {c->ev_upd, c->ev_grad_src, c->ev_grad_copied})
@@ -687,8 +691,10 @@ static gck_status submit_direct(gck_ctx *c, uint32_t i, const gck_step_args *a, 
         void *dst[1] = {c->glog[i - 1]};
         void *dd[1] = {c->arena_dev + ((char *)c->glog[i - 1] - c->arena)};
         const uint64_t bytes[1] = {ghi * 2};
+        if (c->cfg.timing) cudaEventRecord(c->ev_g0[i - 1], c->d2h);
         const int r = drain_sections(c->cfg.copy_mode, src, dst, dd, bytes, 1, c->cfg.chunk_bytes, c->cfg.zc_ctas,
                                      c->d2h);
+        if (c->cfg.timing) cudaEventRecord(c->ev_g1[i - 1], c->d2h);
         if (r < 0 || cudaEventRecord(c->ev_grad_copied, c->d2h) != cudaSuccess) {
             c->abort_session(cudaGetLastError(), "direct: gradient copy");
             return GCK_E_ABORTED;

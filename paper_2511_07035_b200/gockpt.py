@@ -146,6 +146,15 @@ def load_checkpoint(path: str, n: int, threads: int = 0):
     return out[0], out[1], out[2], _hdr_dict(h), st.as_dict()
 
 
+def recommend_k(n: int, link_gbs: float, t_step_s: float, budget: float = 1.0, k_max: int = 16, A: int = 1024):
+    """NEXT-4 (gck_recommend_k) -> (K, V_max bytes); K = 0 if none fits."""
+    k, vmax = C.c_uint32(0), C.c_double(0)
+    st = lib().gck_recommend_k(n, A, link_gbs, t_step_s, budget, k_max, C.byref(k), C.byref(vmax))
+    if st not in (L.OK, L.E_INVALID):
+        check(st)
+    return k.value, vmax.value
+
+
 GEN_MASTER, GEN_EXP_AVG, GEN_EXP_AVG_SQ, GEN_GRAD = 1, 2, 3, 4
 
 
