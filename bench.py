@@ -67,6 +67,10 @@ def parse():
     ap.add_argument("--ring-slots", type=int, default=2)
     ap.add_argument("--staging", default="ring", choices=["ring", "direct"],
                     help="ring: fused kernel packs into an HBM ring; direct: GoCkpt-O literal (no ring)")
+    ap.add_argument("--scheme", default="gockpt", choices=["gockpt", "sync", "async-o"],
+                    help="NEXT-3 baselines in the same harness: sync = blocking D2H snapshot of the full "
+                         "state (DeepSpeed/Async snapshot phase); async-o = the snapshot overlaps the next "
+                         "step's F/B and its update waits for it (P:312-318)")
     ap.add_argument("--replay-threads", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -215,6 +219,10 @@ def main():
     ctx = G.GoCkpt(master, exp_avg, exp_avg_sq, param, **HP, k_min=K, k_max=K, part_align=1024,
                    ring_slots=args.ring_slots, copy_mode=args.copy_mode, replay_threads=args.replay_threads,
                    timing=True, eager_replay=True, staging=args.staging)
+    baseline = args.scheme != "gockpt"
+    if baseline:
+        snap_host = [torch.empty(n, dtype=torch.float32, pin_memory=True) for _ in range(3)]
+        side = torch.cuda.Stream()
     parts = G.plan_parts(n, K, 1024)
     session_bytes = sum(12 * (hi - lo) + (2 * hi if i < K - 1 else 0) for i, (lo, hi) in enumerate(parts))
     state = {"step": 0, "gen": 0}
@@ -236,13 +244,14 @@ def main():
     plain_bytes = 28 * n
     kern = {"plain_ms": [], "plain_bytes": 0, "sess_ms0": 0.0, "sess_n0": 0, "sess_bytes": 0}
 
-    def train_step(part, h_grad=None, time_kernel=False, step_events=None):
+    def train_step(part, h_grad=None, time_kernel=False, step_events=None, snapshot=False):
         state["step"] += 1
         s = state["step"]
         if step_events is not None:
             ev = torch.cuda.Event(enable_timing=True)
             ev.record(stream)
             step_events.append(ev)
+        pre_wait = baseline_snapshot() if snapshot else None   # NEXT-3 baselines: S(t0) = the state now
         fb()                                                           # F/B stand-in
         ctx.grad_fence(stream)   # direct staging: the last gradient slice is out before we overwrite
         if h_grad is not None:
@@ -256,6 +265,8 @@ def main():
         else:
             G.h_generate(G.GEN_GRAD, grad, seed, s, rank * n, 1, 4)    # backward's gradient (harness)
             state["gen"] += 1
+        if pre_wait is not None:      # async-o: the update may not run before the snapshot copy ends
+            stream.wait_event(pre_wait)
         a = b = None
         if time_kernel and part == 0:
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -267,12 +278,30 @@ def main():
         if world > 1:
             dist.all_gather_into_tensor(full_param, param.view(torch.bfloat16))
 
+    def baseline_snapshot():
+        """NEXT-3: snapshot S(t0) of the full state; returns the event the next update must wait on."""
+        srcs = (master, exp_avg, exp_avg_sq)
+        if args.scheme == "sync":
+            for h, d in zip(snap_host, srcs):
+                G.d2h_copy(h, d, stream=stream)        # on the compute stream: training blocks
+            return None
+        ev = torch.cuda.Event()
+        ev.record(stream)
+        side.wait_event(ev)
+        for h, d in zip(snap_host, srcs):
+            G.d2h_copy(h, d, stream=side)
+        done = torch.cuda.Event()
+        done.record(side)
+        return done
+
     def interval(ckpt=True, h_grad=None, time_kernel=False, step_events=None):
         for j in range(1, I + 1):
-            part = j if (ckpt and j <= K) else 0
+            part = j if (ckpt and not baseline and j <= K) else 0
             if part == 1:
                 ctx.begin_checkpoint(state["step"], K)
-            train_step(part, h_grad, time_kernel, step_events)
+            train_step(part, h_grad, time_kernel, step_events, snapshot=ckpt and baseline and j == 1)
+        if ckpt and baseline:
+            return
         if ckpt:
             ck = ctx.finalize()
             assert ck.step == state["step"] - I + K - 1
@@ -311,8 +340,9 @@ def main():
     value = tokens_total / t_ck
     # step times inside the timed region (event deltas); session steps are the first K of each interval
     step_ms = [step_ev[k].elapsed_time(step_ev[k + 1]) for k in range(len(step_ev) - 1)]
-    sess_ms = [t for k, t in enumerate(step_ms) if (k % I) < K]
-    plain_ms_steps = [t for k, t in enumerate(step_ms) if (k % I) >= K]
+    K_aff = 1 if baseline else K      # steps of an interval the checkpoint can delay
+    sess_ms = [t for k, t in enumerate(step_ms) if (k % I) < K_aff]
+    plain_ms_steps = [t for k, t in enumerate(step_ms) if (k % I) >= K_aff]
     kern_plain = [a.elapsed_time(b) for a, b in kern["plain_ms"]]
     kern["plain_ms"] = []
     sess_kernel_ms = st1["kernel_ms_total"] - st0["kernel_ms_total"]
@@ -322,7 +352,7 @@ def main():
     achieved = plain_bytes / plain_mean_s / 1e9
     # session launches additionally write the slot (12|P_i| + 2 hi_i bytes, = the drained bytes)
     sess_alg = args.steps * (K * plain_bytes + session_bytes)
-    sess_achieved = sess_alg / (sess_kernel_ms / 1e3) / 1e9 if sess_kernel_ms > 0 else None
+    sess_achieved = sess_alg / (sess_kernel_ms / 1e3) / 1e9 if sess_kernel_ms > 0 and not baseline else None
     hbm_peak, peak_src = peaks()
     stall_wait_ms = (st1["stall_ms_total"] - st0["stall_ms_total"])
     d2h_bytes = st1["d2h_bytes"] - st0["d2h_bytes"]
@@ -381,7 +411,8 @@ def main():
                    "zero1_degree": args.W,
                    "fb_standin": f"{args.model} fwd+bwd GEMM chain (cuBLAS bf16, CUDA graph)",
                    "fb_tflop_per_step": fb.flops / 1e12, "copy_mode": args.copy_mode,
-                   "ring_slots": args.ring_slots, "staging": args.staging, "parallelism": f"zero1-dp{world}",
+                   "ring_slots": args.ring_slots, "staging": args.staging, "scheme": args.scheme,
+                   "parallelism": f"zero1-dp{world}",
                    "l2": f"inputs larger than L2 ({12 * n / 1e9:.2f} GB fp32 state + {2 * n / 1e9:.2f} GB gradient "
                          f"per step per rank)",
                    "step": "one checkpoint interval (I training steps, one K-part session, finalize)"},

@@ -176,8 +176,7 @@ __device__ __forceinline__ void process4(const FusedArgs &a, const RecF &r, bool
     }
     if (!skip) {
         const uint32_t gb[4] = {g2.x & 0xFFFFu, g2.x >> 16, g2.y & 0xFFFFu, g2.y >> 16};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) adamw_elem_fast(p[k], m[k], v[k], gb[k], r);
+        adamw_group_fast(p, m, v, gb, r);
         *reinterpret_cast<float4 *>(a.p + e) = make_float4(p[0], p[1], p[2], p[3]);
         *reinterpret_cast<float4 *>(a.m + e) = make_float4(m[0], m[1], m[2], m[3]);
         *reinterpret_cast<float4 *>(a.v + e) = make_float4(v[0], v[1], v[2], v[3]);
@@ -332,8 +331,10 @@ __global__ void __launch_bounds__(256) replay_kernel(const ReplayArgs a) {
                 if (a.rec[i].skip) continue;
                 const RecF r = to_recf(a.rec[i]);
                 const uint4 gq = *reinterpret_cast<const uint4 *>(a.glog[i] + e);
+                uint32_t gb[8];
 #pragma unroll
-                for (int k = 0; k < 8; ++k) adamw_elem_fast(p.x[k], m.x[k], v.x[k], bf16_lane(gq, k), r);
+                for (int k = 0; k < 8; ++k) gb[k] = bf16_lane(gq, k);
+                adamw_group_fast(p.x, m.x, v.x, gb, r);
             }
             st8(a.p + e, p);
             st8(a.m + e, m);
@@ -477,9 +478,9 @@ int launch_fused(const FusedArgs &a, bool pack, void *stream, int num_sms) {
     if (aligned && (impl == 2 || (impl == 0 && a.n >= kTmaMinElems))) {
         const int cfg = [] {
             const char *e = getenv("GCK_TMA_CFG");
-            if (!e) return 6116;
+            if (!e) return 4116;
             int st = 0, b = 0, cw = 0;
-            if (sscanf(e, "%d,%d,%d", &st, &b, &cw) != 3) return 6116;
+            if (sscanf(e, "%d,%d,%d", &st, &b, &cw) != 3) return 4116;
             return st * 1000 + b * 100 + cw;
         }();
         switch (cfg) {
@@ -490,7 +491,7 @@ int launch_fused(const FusedArgs &a, bool pack, void *stream, int num_sms) {
             case 3208: return launch_tma<3, 2, 8>(a, pack, s, num_sms);
             case 3216: return launch_tma<3, 2, 16>(a, pack, s, num_sms);
             case 3108: return launch_tma<3, 1, 8>(a, pack, s, num_sms);
-            default: return launch_tma<6, 1, 16>(a, pack, s, num_sms);
+            default: return launch_tma<4, 1, 16>(a, pack, s, num_sms);
         }
     }
     const unsigned grid = grid_for(a.n >> 3, 256, num_sms, 8);
