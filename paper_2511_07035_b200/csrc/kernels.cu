@@ -185,9 +185,10 @@ __device__ __forceinline__ void process4(const FusedArgs &a, const RecF &r, bool
 }
 
 template <bool PACK, int kStages, int kMinBlocks, int kCW>
-__global__ void __launch_bounds__((kCW + 1) * 32, kMinBlocks) fused_adamw_pack_tma_kernel(const FusedArgs a) {
-    // kCW consumer warps; each consumer thread owns kQ float4 groups of the tile:
-    // elements [4(c + q*kCW*32), +4) for q < kQ (coalesced 16-B accesses across the warp).
+__global__ void __launch_bounds__((kCW + 2) * 32, kMinBlocks) fused_adamw_pack_tma_kernel(const FusedArgs a) {
+    // Warps 0..kCW-1 consume (kQ float4 groups of the tile per thread: elements
+    // [4(c + q*kCW*32), +4)); warp kCW produces (bulk loads); warp kCW+1 packs in a session
+    // (bulk stores of the staged tile straight into the ring slot) and idles otherwise.
     constexpr int kThreads = kCW * 32;
     constexpr int kQ = kTile / 4 / kThreads;
     static_assert(kQ * kThreads * 4 == kTile, "tile must split evenly");
@@ -199,7 +200,7 @@ __global__ void __launch_bounds__((kCW + 1) * 32, kMinBlocks) fused_adamw_pack_t
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kCW);
+            mbar_init(&empty[s], kCW + (PACK ? 1 : 0));
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -222,6 +223,41 @@ __global__ void __launch_bounds__((kCW + 1) * 32, kMinBlocks) fused_adamw_pack_t
         }
         return;
     }
+    if (warp == kCW + 1) {  // pack warp (session launches only)
+        if (PACK && lane == 0) {
+            uint32_t k = 0;
+            for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++k) {
+                const int s = k % kStages;
+                const uint32_t ph = (k / kStages) & 1u;
+                mbar_wait(&full[s], ph);
+                const uint8_t *st = smem + s * kStageBytes;
+                const uint64_t base = tile * kTile;
+                // the pre-update p, m, v of the tile's overlap with [lo, hi); g of its overlap with [0, ghi)
+                const uint64_t olo = base > a.lo ? base : a.lo;
+                const uint64_t ohi = (base + kTile) < a.hi ? (base + kTile) : a.hi;
+                const uint64_t ghi = (base + kTile) < a.ghi ? (base + kTile) : a.ghi;
+                bool issued = false;
+                if (olo < ohi) {
+                    const uint32_t off = (uint32_t)(olo - base), bytes = (uint32_t)(ohi - olo) * 4;
+                    bulk_s2g(a.sp + (olo - a.lo), st + off * 4, bytes);
+                    bulk_s2g(a.sm + (olo - a.lo), st + kTile * 4 + off * 4, bytes);
+                    bulk_s2g(a.sv + (olo - a.lo), st + kTile * 8 + off * 4, bytes);
+                    issued = true;
+                }
+                if (base < ghi) {
+                    bulk_s2g(a.sg + base, st + kTile * 12, (uint32_t)(ghi - base) * 2);
+                    issued = true;
+                }
+                if (issued) {
+                    bulk_commit();
+                    bulk_wait_read();  // the stage may be refilled only after the stores read it
+                }
+                mbar_arrive(&empty[s]);
+            }
+            bulk_wait_all();  // slot writes complete before the CTA retires
+        }
+        return;
+    }
     const RecF r = to_recf(a.rec);
     const bool skip = a.rec.skip != 0;
     const int c = threadIdx.x;
@@ -232,26 +268,6 @@ __global__ void __launch_bounds__((kCW + 1) * 32, kMinBlocks) fused_adamw_pack_t
         mbar_wait(&full[s], ph);
         const uint8_t *st = smem + s * kStageBytes;
         const uint64_t base = tile * kTile;
-        if (PACK && c == 0) {
-            // pack with bulk async stores straight from the staged tile (async proxy, no registers):
-            // the pre-update p, m, v of the tile's overlap with [lo, hi) and g of its overlap with [0, ghi)
-            const uint64_t olo = base > a.lo ? base : a.lo;
-            const uint64_t ohi = (base + kTile) < a.hi ? (base + kTile) : a.hi;
-            const uint64_t ghi = (base + kTile) < a.ghi ? (base + kTile) : a.ghi;
-            bool issued = false;
-            if (olo < ohi) {
-                const uint32_t off = (uint32_t)(olo - base), bytes = (uint32_t)(ohi - olo) * 4;
-                bulk_s2g(a.sp + (olo - a.lo), st + off * 4, bytes);
-                bulk_s2g(a.sm + (olo - a.lo), st + kTile * 4 + off * 4, bytes);
-                bulk_s2g(a.sv + (olo - a.lo), st + kTile * 8 + off * 4, bytes);
-                issued = true;
-            }
-            if (base < ghi) {
-                bulk_s2g(a.sg + base, st + kTile * 12, (uint32_t)(ghi - base) * 2);
-                issued = true;
-            }
-            if (issued) bulk_commit();
-        }
         const float4 *sp = reinterpret_cast<const float4 *>(st);
         const float4 *sm = reinterpret_cast<const float4 *>(st + kTile * 4);
         const float4 *sv = reinterpret_cast<const float4 *>(st + kTile * 8);
@@ -265,7 +281,6 @@ __global__ void __launch_bounds__((kCW + 1) * 32, kMinBlocks) fused_adamw_pack_t
             vq[q] = sv[c + q * kThreads];
             gq[q] = sg[c + q * kThreads];
         }
-        if (PACK && c == 0) bulk_wait_read();  // the bulk stores have read the stage
         // Release the stage only once every lane's shared-memory loads have landed in registers:
         // a dependent instruction on all loaded values makes the scoreboard wait for the LDS
         // results, __syncwarp orders the lanes before lane 0's arrive, and the proxy fence orders
@@ -287,7 +302,6 @@ __global__ void __launch_bounds__((kCW + 1) * 32, kMinBlocks) fused_adamw_pack_t
         for (int q = 0; q < kQ; ++q)
             process4(a, r, skip, false, base + 4 * (uint64_t)(c + q * kThreads), pq[q], mq[q], vq[q], gq[q]);
     }
-    if (PACK && c == 0) bulk_wait_all();  // slot writes complete before the CTA retires
     // ragged tail [n_tiles*kTile, n): block 0's consumers, plain loads
     if (blockIdx.x == 0) {
         for (uint64_t e = n_tiles * kTile + (uint64_t)c; e < a.n; e += kThreads) {
@@ -453,7 +467,7 @@ int launch_tma(const FusedArgs &a, bool pack, cudaStream_t s, int num_sms) {
     const uint64_t tiles = a.n / kTile;
     const uint64_t cap = (uint64_t)(num_sms > 0 ? num_sms : 148) * B;
     const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, cap));
-    const unsigned block = (CW + 1) * 32;
+    const unsigned block = (CW + 2) * 32;
     if (pack)
         fused_adamw_pack_tma_kernel<true, S, B, CW><<<grid, block, tma_smem(S), s>>>(a);
     else
