@@ -112,11 +112,13 @@ __global__ void __launch_bounds__(256) fused_adamw_pack_kernel(const FusedArgs a
 }
 
 // ---- TMA-pipelined variant of a2 (the default for n >= kTmaMinElems) ----
-// Persistent CTAs (2 per SM). One producer warp streams tiles of p, m, v (fp32) and g (bf16)
-// into a kStages-deep shared-memory ring with 1-D bulk async copies (cp.async.bulk, SASS
-// UBLKCP) completing on mbarriers; 8 consumer warps compute from shared memory and store
-// p', m', v', bf16(p') (and, in a session, the pre-update slot copy) with 16-B STG. Bytes in
-// flight per SM no longer depend on registers: up to 2 x kStages x 28 KiB.
+// Persistent CTAs (default: 1 per SM, 4 stages, 16 consumer warps; GCK_TMA_CFG selects other
+// instantiations for experiments). One producer warp streams 2048-element tiles of p, m, v
+// (fp32) and g (bf16) into a kStages-deep shared-memory ring with 1-D bulk async copies
+// (cp.async.bulk, SASS UBLKCP.S.G) completing on mbarriers; the consumer warps compute from
+// shared memory (adamw_group_fast) and store p', m', v', bf16(p') with 16-B STG; in a session a
+// pack warp bulk-stores the staged pre-update tile into the ring slot (UBLKCP.G.S). Bytes in
+// flight per SM no longer depend on registers: up to kStages x 28 KiB.
 constexpr int kTile = 2048;                        // elements per tile
 constexpr uint64_t kTmaMinElems = 1u << 18;
 constexpr int kStageBytes = kTile * 14;            // p, m, v fp32 + g bf16
