@@ -1,0 +1,9 @@
+#!/bin/bash
+python -c "import __graft_entry__ as g; g.build()" || exit 1
+mkdir -p gpurun_out
+for tool in memcheck racecheck synccheck initcheck; do
+  echo "== $tool"
+  timeout 900 compute-sanitizer --tool $tool --target-processes all --kernel-name kns=gck \
+      python scripts/sanitize_session.py > gpurun_out/sanitize_$tool.log 2>&1
+  echo "rc=$?"; tail -4 gpurun_out/sanitize_$tool.log
+done
