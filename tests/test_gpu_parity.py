@@ -6,6 +6,8 @@ error of the CPU oracle per element (expected: 0, the op order is pinned).
 Sizes span many 2048-element tiles plus a ragged tail.
 """
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -376,3 +378,19 @@ def test_direct_staging_session(G, n, K, A, copy):
     assert ctx.stats()["d2h_bytes"] == oracle.session_bytes(parts)
     ctx.release()
     ctx.close()
+
+
+# ---------------------------------------------------------------- the boundary from plain C
+def test_c_api_demo_program(G, tmp_path, repo_root):
+    """The ABI is usable from C without Python or torch: build examples/c_api_demo.c with gcc against
+    include/gockpt.h + libgockpt.so, run a session, checkpoint == synchronous snapshot."""
+    import subprocess
+    cuda = os.environ.get("CUDA_HOME", "/usr/local/cuda")
+    exe = str(tmp_path / "c_api_demo")
+    subprocess.run(["gcc", "-O2", "-I", os.path.join(repo_root, "include"), "-I", os.path.join(cuda, "include"),
+                    os.path.join(repo_root, "examples", "c_api_demo.c"), "-L", os.path.dirname(G.LIB_PATH),
+                    "-l:libgockpt.so", "-L", os.path.join(cuda, "lib64"), "-lcudart",
+                    f"-Wl,-rpath,{os.path.dirname(G.LIB_PATH)}", "-o", exe], check=True)
+    for n, K in [((1 << 20) + 7, 4), (124_439_808, 8)]:
+        r = subprocess.run([exe, str(n), str(K)], capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0 and "== the synchronous snapshot" in r.stdout, r.stdout + r.stderr
