@@ -65,13 +65,15 @@ def parse():
     ap.add_argument("--tokens", type=int, default=0, help="tokens per step per rank (0 = model default)")
     ap.add_argument("--copy-mode", default="ce", choices=["ce", "zerocopy"])
     ap.add_argument("--ring-slots", type=int, default=2)
-    ap.add_argument("--staging", default="ring", choices=["ring", "direct"],
-                    help="ring: fused kernel packs into an HBM ring; direct: GoCkpt-O literal (no ring)")
+    ap.add_argument("--staging", default="ring", choices=["ring", "direct", "blocking"],
+                    help="ring: fused kernel packs into an HBM ring; direct: GoCkpt-O literal (no ring); "
+                         "blocking: paper-faithful GoCkpt (the update waits for its gradient slice)")
     ap.add_argument("--scheme", default="gockpt", choices=["gockpt", "sync", "async-o"],
                     help="NEXT-3 baselines in the same harness: sync = blocking D2H snapshot of the full "
                          "state (DeepSpeed/Async snapshot phase); async-o = the snapshot overlaps the next "
                          "step's F/B and its update waits for it (P:312-318)")
-    ap.add_argument("--replay-threads", type=int, default=0)
+    ap.add_argument("--replay-threads", type=int, default=0,
+                    help="host replay / persist threads (0 = the host's cores divided by the local ranks)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=1 << 24,
@@ -199,6 +201,9 @@ def main():
     gbuild.build()
     dev = torch.device("cuda", local)
     n, K, I, T = args.n, args.K, args.interval, args.tokens
+    if not args.replay_threads:   # share the host's cores between the ranks of this node
+        local_world = int(os.environ.get("LOCAL_WORLD_SIZE", "1"))
+        args.replay_threads = max(1, len(os.sched_getaffinity(0)) // max(1, local_world))
     stream = torch.cuda.current_stream()
 
     # ---- state (synthetic warm S(t0), generated on device by the harness generator)

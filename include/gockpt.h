@@ -75,7 +75,7 @@ typedef struct {
 
 enum { GCK_COPY_ENGINE = 0, GCK_COPY_ZEROCOPY = 1 };
 enum { GCK_REPLAY_HOST = 0, GCK_REPLAY_GPU = 1 };
-enum { GCK_STAGE_RING = 0, GCK_STAGE_DIRECT = 1 };
+enum { GCK_STAGE_RING = 0, GCK_STAGE_DIRECT = 1, GCK_STAGE_BLOCKING = 2 };
 
 typedef struct {
     uint32_t abi_version;   /* must be GCK_ABI_VERSION */
@@ -101,7 +101,10 @@ typedef struct {
                                GCK_STAGE_DIRECT (GoCkpt-O literal; NEXT-2): no ring — part
                                i is copied from the live arrays while step t0+i's F/B runs (the update
                                waits for it) and G(t0+i)[0:hi_i] from the caller's gradient buffer,
-                               which the caller must not overwrite before gck_grad_fence. */
+                               which the caller must not overwrite before gck_grad_fence.
+                               GCK_STAGE_BLOCKING: the paper-faithful GoCkpt — as DIRECT,
+                               but each update also waits until its gradient slice is on the host
+                               (NEXT-3 comparison scheme). */
 } gck_config;
 
 /* Caller-owned device tensors (PyTorch owns them; they must outlive the context). */

@@ -24,7 +24,7 @@ STATUS_NAMES = ["GCK_OK", "GCK_E_INVALID", "GCK_E_PROTOCOL", "GCK_E_STALE", "GCK
                 "GCK_E_INCOMPLETE", "GCK_E_ABORTED", "GCK_E_BUSY", "GCK_E_NODEVICE", "GCK_E_IO", "GCK_E_CORRUPT"]
 COPY_ENGINE, COPY_ZEROCOPY = 0, 1
 REPLAY_HOST, REPLAY_GPU = 0, 1
-STAGE_RING, STAGE_DIRECT = 0, 1
+STAGE_RING, STAGE_DIRECT, STAGE_BLOCKING = 0, 1, 2
 
 
 class Hparams(C.Structure):

@@ -134,6 +134,7 @@ struct gck_ctx {
     cudaStream_t d2h = nullptr;
     // direct staging (GoCkpt-O literal, NEXT-2): no ring; state D2H straight from the live arrays
     bool direct = false;
+    bool blocking_grad = false;     // paper-faithful GoCkpt: the update waits for its gradient slice
     bool upd_recorded = false;      // ev_upd holds the last fused kernel's completion
     bool grad_copy_recorded = false;
     cudaEvent_t ev_upd{}, ev_grad_src{}, ev_grad_copied{};
@@ -426,7 +427,8 @@ gck_status gck_create(const gck_config *cfg_in, const gck_hparams *hp, const gck
     if (cfg.part_align % 8) return set_tls(GCK_E_INVALID, "part_align must be a multiple of 8");
     if (cfg.k_max < cfg.k_min || cfg.k_max > GCK_K_LIMIT) return set_tls(GCK_E_INVALID, "need 1 <= k_min <= k_max <= 64");
     if (cfg.ring_slots > 2) return set_tls(GCK_E_INVALID, "ring_slots must be 1 or 2");
-    if (cfg.staging != GCK_STAGE_RING && cfg.staging != GCK_STAGE_DIRECT) return set_tls(GCK_E_INVALID, "bad staging");
+    if (cfg.staging != GCK_STAGE_RING && cfg.staging != GCK_STAGE_DIRECT && cfg.staging != GCK_STAGE_BLOCKING)
+        return set_tls(GCK_E_INVALID, "bad staging");
     if (cfg.copy_mode != GCK_COPY_ENGINE && cfg.copy_mode != GCK_COPY_ZEROCOPY)
         return set_tls(GCK_E_INVALID, "bad copy_mode");
     if (cfg.replay_mode != GCK_REPLAY_HOST) return set_tls(GCK_E_INVALID, "replay_mode: only GCK_REPLAY_HOST at finalize (GPU replay: gck_replay_gpu)");
@@ -467,7 +469,8 @@ gck_status gck_create(const gck_config *cfg_in, const gck_hparams *hp, const gck
         }
         glog_max = std::max(glog_max, gsum);
     }
-    c->direct = (cfg.staging == GCK_STAGE_DIRECT);
+    c->direct = (cfg.staging == GCK_STAGE_DIRECT || cfg.staging == GCK_STAGE_BLOCKING);
+    c->blocking_grad = (cfg.staging == GCK_STAGE_BLOCKING);
     c->slot_bytes = c->direct ? 0 : slot_max;
     c->glog_elems_cap = glog_max;
     cudaError_t e = c->direct ? cudaSuccess : cudaMalloc((void **)&c->ring, c->slot_bytes * c->R);
@@ -704,9 +707,12 @@ static gck_status submit_direct(gck_ctx *c, uint32_t i, const gck_step_args *a, 
         c->stats.d2h_bytes += ghi * 2;
         c->stats.last_session_d2h_bytes += ghi * 2;
     }
-    // a4 (direct): the update may not overwrite part i before its state copy has been taken
+    // a4 (direct): the update may not overwrite part i before its state copy has been taken;
+    // paper-faithful GoCkpt additionally blocks until this step's gradient slice is on the host
+    // ("the only visible overhead to the user is the gradient transfer")
     if (c->cfg.timing) cudaEventRecord(c->ev_w0[i - 1], s);
-    const bool ck_ok = cudaStreamWaitEvent(s, c->ev_state_copied[i - 1], 0) == cudaSuccess;
+    bool ck_ok = cudaStreamWaitEvent(s, c->ev_state_copied[i - 1], 0) == cudaSuccess;
+    if (ck_ok && c->blocking_grad && i < c->K) ck_ok = cudaStreamWaitEvent(s, c->ev_grad_copied, 0) == cudaSuccess;
     if (c->cfg.timing) cudaEventRecord(c->ev_w1[i - 1], s);
     int le = gck::launch_fused(f, false, s, c->num_sms);
     if (le) return c->cuda_fail((cudaError_t)le, "fused kernel launch");

@@ -191,7 +191,7 @@ class GoCkpt:
         cfg = L.Config(L.ABI_VERSION, master.device.index or 0, n, k_min, k_max, part_align, ring_slots,
                        {"ce": L.COPY_ENGINE, "zerocopy": L.COPY_ZEROCOPY}[copy_mode], chunk_bytes, zc_ctas,
                        L.REPLAY_HOST, replay_threads, int(timing), int(eager_replay),
-                       {"ring": L.STAGE_RING, "direct": L.STAGE_DIRECT}[staging])
+                       {"ring": L.STAGE_RING, "direct": L.STAGE_DIRECT, "blocking": L.STAGE_BLOCKING}[staging])
         hp = L.Hparams(beta1, beta2, eps, weight_decay)
         self.hparams = dict(beta1=beta1, beta2=beta2, eps=eps, weight_decay=weight_decay)
         t = L.Tensors(_dptr(master), _dptr(exp_avg), _dptr(exp_avg_sq), _dptr(param_bf16))

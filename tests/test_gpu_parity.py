@@ -333,9 +333,10 @@ def test_persist_restore_resume_equals_uninterrupted(G, tmp_path):
 
 
 # ---------------------------------------------------------------- NEXT-2: direct staging (GoCkpt-O literal)
-@pytest.mark.parametrize("n,K,A,copy", [(1 << 20, 4, 1024, "ce"), (1_000_003, 8, 1024, "ce"),
-                                        (300_007, 3, 8, "zerocopy"), (1 << 20, 1, 1024, "ce")])
-def test_direct_staging_session(G, n, K, A, copy):
+@pytest.mark.parametrize("n,K,A,copy,staging", [(1 << 20, 4, 1024, "ce", "direct"), (1_000_003, 8, 1024, "ce", "direct"),
+                                                (300_007, 3, 8, "zerocopy", "direct"), (1 << 20, 1, 1024, "ce", "direct"),
+                                                (1_000_003, 4, 1024, "ce", "blocking")])
+def test_direct_staging_session(G, n, K, A, copy, staging):
     """No HBM ring: part i is copied from the live arrays during step t0+i's F/B, the gradient
     prefix from ONE reused gradient buffer that the 'backward' overwrites right after
     gck_grad_fence. Staged bytes, host replay, GPU replay and snapshot as in ring mode."""
@@ -343,7 +344,7 @@ def test_direct_staging_session(G, n, K, A, copy):
     state, grads, recs, sargs = session_inputs(seed, n, K, t0)
     p, m, v = (up_f32(x) for x in state)
     ctx = G.GoCkpt(p, m, v, None, **HP, k_min=1, k_max=max(K, 8), part_align=A, copy_mode=copy,
-                   eager_replay=False, staging="direct")
+                   eager_replay=False, staging=staging)
     gbuf = torch.empty(n, dtype=torch.int16, device="cuda")
     for s in range(1, 3):                                   # plain steps before the session
         gbuf.copy_(up_u16(gi.grad_bits(seed, 1000 + s, n)))
