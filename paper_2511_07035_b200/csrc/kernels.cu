@@ -119,10 +119,8 @@ __global__ void __launch_bounds__(256) fused_adamw_pack_kernel(const FusedArgs a
 // shared memory (adamw_group_fast) and store p', m', v', bf16(p') with 16-B STG; in a session a
 // pack warp bulk-stores the staged pre-update tile into the ring slot (UBLKCP.G.S). Bytes in
 // flight per SM no longer depend on registers: up to kStages x 28 KiB.
-constexpr int kTile = 2048;                        // elements per tile
 constexpr uint64_t kTmaMinElems = 1u << 18;
-constexpr int kStageBytes = kTile * 14;            // p, m, v fp32 + g bf16
-constexpr int tma_smem(int stages) { return stages * kStageBytes + 2 * stages * 8; }
+constexpr int tma_smem(int stages, int tile) { return stages * tile * 14 + 2 * stages * 8; }
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -186,12 +184,13 @@ __device__ __forceinline__ void process4(const FusedArgs &a, const RecF &r, bool
     if (a.out) *reinterpret_cast<uint2 *>(a.out + e) = make_uint2(pack_bf16x2(p[0], p[1]), pack_bf16x2(p[2], p[3]));
 }
 
-template <bool PACK, int kStages, int kMinBlocks, int kCW>
+template <bool PACK, int kStages, int kMinBlocks, int kCW, int kTile>
 __global__ void __launch_bounds__((kCW + 2) * 32, kMinBlocks) fused_adamw_pack_tma_kernel(const FusedArgs a) {
     // Warps 0..kCW-1 consume (kQ float4 groups of the tile per thread: elements
     // [4(c + q*kCW*32), +4)); warp kCW produces (bulk loads); warp kCW+1 packs in a session
     // (bulk stores of the staged tile straight into the ring slot) and idles otherwise.
     constexpr int kThreads = kCW * 32;
+    constexpr int kStageBytes = kTile * 14;  // p, m, v fp32 + g bf16
     constexpr int kQ = kTile / 4 / kThreads;
     static_assert(kQ * kThreads * 4 == kTile, "tile must split evenly");
     extern __shared__ __align__(128) uint8_t smem[];
@@ -456,29 +455,27 @@ inline unsigned grid_for(uint64_t work_items, unsigned block, int num_sms, unsig
 
 }  // namespace
 
-template <int S, int B, int CW>
+template <int S, int B, int CW, int TL = 2048>
 int launch_tma(const FusedArgs &a, bool pack, cudaStream_t s, int num_sms) {
     static bool attr_set = false;
     if (!attr_set) {
-        cudaFuncSetAttribute(fused_adamw_pack_tma_kernel<true, S, B, CW>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(S));
-        cudaFuncSetAttribute(fused_adamw_pack_tma_kernel<false, S, B, CW>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(S));
+        cudaFuncSetAttribute(fused_adamw_pack_tma_kernel<true, S, B, CW, TL>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(S, TL));
+        cudaFuncSetAttribute(fused_adamw_pack_tma_kernel<false, S, B, CW, TL>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(S, TL));
         attr_set = true;
     }
-    const uint64_t tiles = a.n / kTile;
+    const uint64_t tiles = a.n / TL;
     const uint64_t cap = (uint64_t)(num_sms > 0 ? num_sms : 148) * B;
     const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, cap));
     const unsigned block = (CW + 2) * 32;
     if (pack)
-        fused_adamw_pack_tma_kernel<true, S, B, CW><<<grid, block, tma_smem(S), s>>>(a);
+        fused_adamw_pack_tma_kernel<true, S, B, CW, TL><<<grid, block, tma_smem(S, TL), s>>>(a);
     else
-        fused_adamw_pack_tma_kernel<false, S, B, CW><<<grid, block, tma_smem(S), s>>>(a);
+        fused_adamw_pack_tma_kernel<false, S, B, CW, TL><<<grid, block, tma_smem(S, TL), s>>>(a);
     return (int)cudaGetLastError();
 }
 
-// Kernel-variant overrides for experiments and differential tests, read at every launch:
-// GCK_FUSED_IMPL = "simple" | "tma", GCK_TMA_CFG = "stages,blocks_per_sm,consumer_warps".
 int fused_impl_default() {
     const char *e = getenv("GCK_FUSED_IMPL");
     if (e && e[0] == 's') return 1;
@@ -507,6 +504,8 @@ int launch_fused(const FusedArgs &a, bool pack, void *stream, int num_sms) {
             case 3208: return launch_tma<3, 2, 8>(a, pack, s, num_sms);
             case 3216: return launch_tma<3, 2, 16>(a, pack, s, num_sms);
             case 3108: return launch_tma<3, 1, 8>(a, pack, s, num_sms);
+            case 4124: return launch_tma<4, 1, 24, 3072>(a, pack, s, num_sms);
+            case 3130: return launch_tma<3, 1, 30, 3840>(a, pack, s, num_sms);
             default: return launch_tma<4, 1, 16>(a, pack, s, num_sms);
         }
     }
