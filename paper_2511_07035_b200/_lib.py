@@ -13,7 +13,9 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgockpt.so")
+# GCK_LIB_PATH selects another build of the same library (e.g. the ASan/UBSan build of
+# scripts/build_asan.sh); the default is the in-tree sm_100a build.
+LIB_PATH = os.environ.get("GCK_LIB_PATH") or os.path.join(_HERE, "libgockpt.so")
 
 ABI_VERSION = 1
 K_LIMIT = 64
