@@ -246,6 +246,7 @@ def main():
     link_peak = (1 << 30) / best / 1e6
     del link, link_h
 
+    result_host = []
     plain_bytes = 28 * n
     kern = {"plain_ms": [], "plain_bytes": 0, "sess_ms0": 0.0, "sess_n0": 0, "sess_bytes": 0}
 
@@ -373,6 +374,7 @@ def main():
     # ---- e2e: gradient from pinned host memory each step, result = the host checkpoint
     e2e = None
     if not args.no_e2e:
+        result_host[:] = [torch.empty(4, dtype=torch.int16, pin_memory=True) for _ in range(2)]
         h_grads = [torch.empty(n, dtype=torch.int16, pin_memory=True) for _ in range(2)]
         for k, hg in enumerate(h_grads):
             tmp = torch.empty(n, dtype=torch.int16, device=dev)
@@ -383,10 +385,11 @@ def main():
         interval(ckpt=True, h_grad=h_grads)   # warm the path
         t_e2e = timed(max(1, args.steps), ckpt=True, h_grad=h_grads)
         e2e = {"value": max(1, args.steps) * I * T * world / t_e2e, "unit": "tokens/s",
-               "h2d_bytes_per_step": 2 * n, "d2h_bytes_per_step": session_bytes / I,
+               "h2d_bytes_per_step": 2 * n, "d2h_bytes_per_step": 8 + session_bytes / I,
                "note": "the reduced bf16 gradient shard arrives by H2D from pinned host memory every step "
-                       "(compute stream, inside the timed region; replaces generator + reduce-scatter); the "
-                       "step's result is the host checkpoint the library drains (D2H)"}
+                       "(compute stream, inside the timed region; replaces generator + reduce-scatter); each "
+                       "step reads 8 bytes of the updated params back (the step's result), and the "
+                       "checkpoint the library drains is the session's result (D2H)"}
 
     # ---- oracle on host cores (rank 0, N=1 only)
     cpu = None
