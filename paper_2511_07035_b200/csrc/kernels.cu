@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 
@@ -457,13 +458,16 @@ inline unsigned grid_for(uint64_t work_items, unsigned block, int num_sms, unsig
 
 template <int S, int B, int CW, int TL = 2048>
 int launch_tma(const FusedArgs &a, bool pack, cudaStream_t s, int num_sms) {
-    static bool attr_set = false;
-    if (!attr_set) {
+    static std::atomic<uint64_t> attr_set_devices{0};  // the smem opt-in is per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(attr_set_devices.load() & bit)) {
         cudaFuncSetAttribute(fused_adamw_pack_tma_kernel<true, S, B, CW, TL>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(S, TL));
         cudaFuncSetAttribute(fused_adamw_pack_tma_kernel<false, S, B, CW, TL>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, tma_smem(S, TL));
-        attr_set = true;
+        attr_set_devices.fetch_or(bit);
     }
     const uint64_t tiles = a.n / TL;
     const uint64_t cap = (uint64_t)(num_sms > 0 ? num_sms : 148) * B;
