@@ -12,6 +12,7 @@ import subprocess
 import sys
 
 rep, launches, tag, n = sys.argv[1], sys.argv[2], sys.argv[3], int(sys.argv[4])
+out_launches = sys.argv[5] if len(sys.argv) > 5 else f"profiles/{tag}_launches.txt"
 METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
            "dram__throughput.avg.pct_of_peak_sustained_elapsed",
@@ -19,8 +20,8 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "launch__grid_size", "launch__block_size", "sm__warps_active.avg.pct_of_peak_sustained_active",
            "smsp__issue_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum",
            "lts__t_bytes.sum", "l1tex__t_bytes.sum"]
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
-rows = list(csv.reader(io.StringIO(raw)))
+raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout if rep != "-" else ""
+rows = list(csv.reader(io.StringIO(raw))) or [[], []]
 hdr, units = rows[0], rows[1]
 out, recs = [], []
 for r in rows[2:]:
@@ -49,8 +50,9 @@ plain = [x for x in js["launches"] if not x["pack"]]
 if plain:
     js["dram_bytes_per_launch"] = plain[0]["dram_read"] + plain[0]["dram_write"]
     js["note"] = "traffic of the plain (no-pack) launch, the dominant launch kind of a checkpoint interval"
-open(f"profiles/{tag}_fused_adamw_pack_ncu.txt", "w").write("\n".join(lines) + "\n")
-json.dump(js, open("profiles/fused_adamw_pack_ncu.json", "w"), indent=1)
+if rep != "-":
+    open(f"profiles/{tag}_fused_adamw_pack_ncu.txt", "w").write("\n".join(lines) + "\n")
+    json.dump(js, open("profiles/fused_adamw_pack_ncu.json", "w"), indent=1)
 
 rows = list(csv.reader(open(launches)))
 hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
@@ -70,6 +72,6 @@ for k, v in sorted(tot.items(), key=lambda x: -x[1]):
     L.append(f"{v / 1e3:10.2f} ms {100 * v / T:6.2f}%  n={cnt[k]:6d}  mean {v / cnt[k]:9.1f} us  {k}")
 gck = sum(v for k, v in tot.items() if "gck::" in k)
 L.insert(1, f"share of our kernels (gck::*): {100 * gck / T:.2f}% of GPU time")
-open(f"profiles/{tag}_launches.txt", "w").write("\n".join(L) + "\n")
+open(out_launches, "w").write("\n".join(L) + "\n")
 print("\n".join(lines[:12]))
 print("\n".join(L[:6]))
