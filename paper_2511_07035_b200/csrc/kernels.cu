@@ -335,6 +335,14 @@ __device__ __forceinline__ uint32_t part_of(const ReplayArgs &a, uint64_t e) {
 }
 
 __global__ void __launch_bounds__(256) replay_kernel(const ReplayArgs a) {
+    // the K step records with their hoisted reciprocals, computed once per CTA
+    __shared__ RecF srec[GCK_K_LIMIT];
+    __shared__ int sskip[GCK_K_LIMIT];
+    for (uint32_t i = threadIdx.x; i < a.K; i += blockDim.x) {
+        srec[i] = to_recf(a.rec[i]);
+        sskip[i] = a.rec[i].skip;
+    }
+    __syncthreads();
     const uint64_t ngroups = (a.n_replay + 7) >> 3;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     for (uint64_t gi = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < ngroups; gi += stride) {
@@ -343,14 +351,16 @@ __global__ void __launch_bounds__(256) replay_kernel(const ReplayArgs a) {
         const bool full = (e + 8 <= a.hi[j]) && (e + 8 <= a.n_replay);
         if (full) {
             Vec8 p = ld8(a.p + e), m = ld8(a.m + e), v = ld8(a.v + e);
+            // software pipeline: the next step's gradient vector is in flight while this step computes
+            uint4 gnext = (j + 1 < a.K) ? *reinterpret_cast<const uint4 *>(a.glog[j] + e) : make_uint4(0, 0, 0, 0);
             for (uint32_t i = j; i + 1 < a.K; ++i) {  // updates t0+j+1 .. t0+K-1 (1-based: j+1..K-1)
-                if (a.rec[i].skip) continue;
-                const RecF r = to_recf(a.rec[i]);
-                const uint4 gq = *reinterpret_cast<const uint4 *>(a.glog[i] + e);
+                const uint4 gq = gnext;
+                if (i + 2 < a.K) gnext = *reinterpret_cast<const uint4 *>(a.glog[i + 1] + e);
+                if (sskip[i]) continue;
                 uint32_t gb[8];
 #pragma unroll
                 for (int k = 0; k < 8; ++k) gb[k] = bf16_lane(gq, k);
-                adamw_group_fast(p.x, m.x, v.x, gb, r);
+                adamw_group_fast(p.x, m.x, v.x, gb, srec[i]);
             }
             st8(a.p + e, p);
             st8(a.m + e, m);
