@@ -198,7 +198,9 @@ gck_status gck_begin_checkpoint(gck_ctx *ctx, uint64_t t0, uint32_t K);
  * packs part i (pre-update) and G[0:hi_i] into the slot and applies the
  * update (a2), then the D2H stream drains the slot into pinned memory (a3).
  * Errors: INVALID, PROTOCOL, STALE, CUDA (kernel launch failure poisons ctx),
- * ABORTED (the checkpoint path failed earlier; the update still ran). */
+ * ABORTED (the checkpoint path failed — now or earlier in this session; the update still ran
+ * as a plain step, the session is void: gck_finalize reports ABORTED, gck_begin_checkpoint
+ * starts a new one). Test hook: GCK_FAULT_DRAIN=<i> fails the drain of session step i. */
 gck_status gck_submit(gck_ctx *ctx, uint32_t part, const gck_step_args *args, void *stream);
 
 /* Direct staging: make `stream` wait until the gradient slice of the latest session step has

@@ -20,6 +20,7 @@
 #include <chrono>
 #include <condition_variable>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <new>
@@ -644,8 +645,15 @@ static int drain_sections(int mode, const void *const *src, void *const *dst, vo
     return 0;
 }
 
+// Fault injection for the abort-path tests: GCK_FAULT_DRAIN=<i> fails the drain of session step i.
+static bool drain_fault(uint32_t i) {
+    const char *e = getenv("GCK_FAULT_DRAIN");
+    return e && (uint32_t)strtoul(e, nullptr, 10) == i;
+}
+
 static gck_status enqueue_drain(gck_ctx *c, uint32_t i, const SlotLayout &L, char *slot) {
     // slot -> host ckpt arrays at offset lo_i, gradient -> glog[i]
+    if (drain_fault(i)) return GCK_E_ABORTED;
     const uint64_t lo = c->lo[i - 1], pe = c->hi[i - 1] - lo;
     const uint64_t ghi = (i < c->K) ? c->hi[i - 1] : 0;
     const void *src[4] = {slot, slot + L.off_m, slot + L.off_v, slot + L.off_g};
@@ -727,7 +735,9 @@ static gck_status submit_direct(gck_ctx *c, uint32_t i, const gck_step_args *a, 
     }
     c->recs[i - 1] = rec;
     if (i < c->K) {  // part i+1 = S(t0+i): copy it while step t0+i+1's F/B runs
-        if ((e = cudaStreamWaitEvent(c->d2h, c->ev_upd, 0)) != cudaSuccess || (e = enqueue_state_copy(c, i + 1)) != cudaSuccess) {
+        if (drain_fault(i)) e = cudaErrorUnknown;
+        else if ((e = cudaStreamWaitEvent(c->d2h, c->ev_upd, 0)) == cudaSuccess) e = enqueue_state_copy(c, i + 1);
+        if (e != cudaSuccess) {
             c->abort_session(e, "direct: state copy");
             return GCK_E_ABORTED;
         }
@@ -756,11 +766,18 @@ gck_status gck_submit(gck_ctx *c, uint32_t part, const gck_step_args *a, void *s
     if (!a->skip && a->adam_t == 0) return c->fail(GCK_E_INVALID, "adam_t must be >= 1");
     const bool in_session = (c->state == State::ACTIVE);
     if (part == 0 && in_session) return c->fail(GCK_E_PROTOCOL, "plain submit inside an active session");
+    bool aborted_note = false;
     if (part != 0) {
-        if (!in_session) return c->fail(c->state == State::ABORTED ? GCK_E_ABORTED : GCK_E_PROTOCOL,
-                                        "session submit without an active session");
-        if (part != c->next_part || a->step != c->t0 + part)
-            return c->fail(GCK_E_STALE, "part must be the next part and step == t0 + part");
+        if (c->state == State::ABORTED) {
+            // the checkpoint path failed earlier in this session: training continues — run the
+            // update as a plain step and report the abort
+            part = 0;
+            aborted_note = true;
+        } else {
+            if (!in_session) return c->fail(GCK_E_PROTOCOL, "session submit without an active session");
+            if (part != c->next_part || a->step != c->t0 + part)
+                return c->fail(GCK_E_STALE, "part must be the next part and step == t0 + part");
+        }
     }
     DeviceGuard g(c->cfg.device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -788,7 +805,7 @@ gck_status gck_submit(gck_ctx *c, uint32_t part, const gck_step_args *a, void *s
             cudaEventRecord(c->ev_upd, s);
             c->upd_recorded = true;
         }
-        return GCK_OK;
+        return aborted_note ? c->fail(GCK_E_ABORTED, c->last_error) : GCK_OK;
     }
     if (c->direct) return submit_direct(c, part, a, s, f, rec, count_before);
 

@@ -395,3 +395,48 @@ def test_c_api_demo_program(G, tmp_path, repo_root):
     for n, K in [((1 << 20) + 7, 4), (124_439_808, 8)]:
         r = subprocess.run([exe, str(n), str(K)], capture_output=True, text=True, timeout=300)
         assert r.returncode == 0 and "== the synchronous snapshot" in r.stdout, r.stdout + r.stderr
+
+
+# ---------------------------------------------------------------- failure path: checkpoint aborted, training continues
+@pytest.mark.parametrize("staging", ["ring", "direct"])
+def test_drain_failure_aborts_checkpoint_not_training(G, staging):
+    """a transfer-channel failure aborts the checkpoint (finalize reports it)
+    while every optimizer update still runs; the next session works normally."""
+    from paper_2511_07035_b200 import GckError
+    from paper_2511_07035_b200 import _lib as L
+    n, K, t0, seed = 300_007, 4, 10, 13
+    state, grads, recs, sargs = session_inputs(seed, n, 2 * K, t0)
+    p, m, v = (up_f32(x) for x in state)
+    ctx = G.GoCkpt(p, m, v, None, **HP, k_min=K, k_max=K, part_align=64, staging=staging)
+    os.environ["GCK_FAULT_DRAIN"] = "2"
+    try:
+        ctx.begin_checkpoint(t0, K)
+        statuses = []
+        for i in range(1, K + 1):
+            a = sargs[i - 1]
+            try:
+                ctx.submit(i, a["step"], a["adam_t"], a["lr"], up_u16(grads[i - 1]), a["grad_scale"], a["skip"])
+                statuses.append(L.OK)
+            except GckError as e:
+                statuses.append(e.status)
+    finally:
+        os.environ.pop("GCK_FAULT_DRAIN", None)
+    assert statuses[0] == L.OK and all(s_ == L.E_ABORTED for s_ in statuses[1:]), statuses
+    with pytest.raises(GckError) as e:
+        ctx.finalize()
+    assert e.value.status == L.E_ABORTED
+    torch.cuda.synchronize()
+    traj = oracle.trajectory(*state, grads, recs)
+    assert_state_equal((down_f32(p), down_f32(m), down_f32(v)), traj[K], "training continued through the abort")
+    # the next session (steps t0+K+1 .. t0+2K) checkpoints normally
+    ctx.begin_checkpoint(t0 + K, K)
+    for i in range(1, K + 1):
+        a = sargs[K + i - 1]
+        if i == K:
+            snap = ctx.sync_snapshot()
+        ctx.submit(i, a["step"], a["adam_t"], a["lr"], up_u16(grads[K + i - 1]), a["grad_scale"], a["skip"])
+    ck = ctx.finalize()
+    assert_state_equal((ck.master, ck.exp_avg, ck.exp_avg_sq), snap, "session after the abort")
+    assert_state_equal((ck.master, ck.exp_avg, ck.exp_avg_sq), traj[2 * K - 1], "session after the abort vs oracle")
+    ctx.release()
+    ctx.close()
