@@ -105,6 +105,10 @@ typedef struct {
                                GCK_STAGE_BLOCKING: the paper-faithful GoCkpt — as DIRECT,
                                but each update also waits until its gradient slice is on the host
                                (NEXT-3 comparison scheme). */
+    int32_t numa_node;      /* host placement of the pinned arena and of the replay/persist threads:
+                               >= 0 binds them to that NUMA node; -1 = the GPU's own node (from its PCI
+                               address; no binding if the platform reports none); -2 = no binding.
+                               P:401: "28 cores per process, same NUMA domain". */
 } gck_config;
 
 /* Caller-owned device tensors (PyTorch owns them; they must outlive the context). */
@@ -168,7 +172,7 @@ typedef struct {
     uint64_t last_session_d2h_bytes;
     uint64_t gpu_launches;         /* kernels this context launched */
     int32_t replay_threads;
-    int32_t _pad;
+    int32_t numa_node;             /* node the arena and threads are bound to (-1: unbound) */
 } gck_stats;
 
 /* ---- context lifecycle -------------------------------------------------- */

@@ -38,7 +38,8 @@ class Config(C.Structure):
                 ("k_min", C.c_uint32), ("k_max", C.c_uint32), ("part_align", C.c_uint32),
                 ("ring_slots", C.c_uint32), ("copy_mode", C.c_int32), ("chunk_bytes", C.c_uint64),
                 ("zc_ctas", C.c_uint32), ("replay_mode", C.c_int32), ("replay_threads", C.c_int32),
-                ("timing", C.c_int32), ("eager_replay", C.c_int32), ("staging", C.c_int32)]
+                ("timing", C.c_int32), ("eager_replay", C.c_int32), ("staging", C.c_int32),
+                ("numa_node", C.c_int32)]
 
 
 class Tensors(C.Structure):
@@ -77,7 +78,7 @@ class Stats(C.Structure):
                 ("d2h_ms_total", C.c_double), ("last_session_stall_ms", C.c_double),
                 ("last_session_d2h_ms", C.c_double), ("last_replay_ms", C.c_double), ("last_worker_ms", C.c_double),
                 ("last_finalize_wait_ms", C.c_double), ("last_session_d2h_bytes", C.c_uint64),
-                ("gpu_launches", C.c_uint64), ("replay_threads", C.c_int32), ("_pad", C.c_int32)]
+                ("gpu_launches", C.c_uint64), ("replay_threads", C.c_int32), ("numa_node", C.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_ if not k.startswith("_")}

@@ -15,6 +15,9 @@
 //  - finalize returning the consistent checkpoint S(t0+K-1) (a6).
 #include <cuda_runtime.h>
 #include <sched.h>
+#include <sys/mman.h>
+#include <sys/syscall.h>
+#include <unistd.h>
 
 #include <atomic>
 #include <chrono>
@@ -107,6 +110,63 @@ void fill_record(double beta1, double beta2, double eps, double wd, double pow1,
     out->t = t;
 }
 
+
+// ---- NUMA placement of the pinned arena and host threads ----------------------------
+int gpu_numa_node(int device) {
+    char bus[64] = {0};
+    if (cudaDeviceGetPCIBusId(bus, sizeof(bus), device) != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
+    for (char *q = bus; *q; ++q) *q = (char)tolower(*q);
+    std::string path = std::string("/sys/bus/pci/devices/") + bus + "/numa_node";
+    FILE *f = fopen(path.c_str(), "r");
+    if (!f) return -1;
+    int node = -1;
+    if (fscanf(f, "%d", &node) != 1) node = -1;
+    fclose(f);
+    return node;
+}
+
+bool node_cpus(int node, cpu_set_t *out) {
+    CPU_ZERO(out);
+    std::string path = "/sys/devices/system/node/node" + std::to_string(node) + "/cpulist";
+    FILE *f = fopen(path.c_str(), "r");
+    if (!f) return false;
+    char buf[4096] = {0};
+    const bool ok = fgets(buf, sizeof(buf), f) != nullptr;
+    fclose(f);
+    if (!ok) return false;
+    int any = 0;
+    for (char *tok = strtok(buf, ",\n"); tok; tok = strtok(nullptr, ",\n")) {
+        int a = -1, b = -1;
+        if (sscanf(tok, "%d-%d", &a, &b) == 2) {
+            for (int c = a; c <= b && c < CPU_SETSIZE; ++c) CPU_SET(c, out), ++any;
+        } else if (sscanf(tok, "%d", &a) == 1 && a < CPU_SETSIZE) {
+            CPU_SET(a, out);
+            ++any;
+        }
+    }
+    return any > 0;
+}
+
+// mmap + mbind(MPOL_BIND) + cudaHostRegister: pinned pages placed on `node`.
+void *alloc_pinned_on_node(uint64_t bytes, int node, bool *registered) {
+    *registered = false;
+    void *p = mmap(nullptr, bytes, PROT_READ | PROT_WRITE, MAP_PRIVATE | MAP_ANONYMOUS, -1, 0);
+    if (p == MAP_FAILED) return nullptr;
+    unsigned long mask[16] = {0};
+    if (node >= 0 && node < 1024) mask[node / (8 * sizeof(unsigned long))] |= 1ul << (node % (8 * sizeof(unsigned long)));
+    syscall(SYS_mbind, p, bytes, 2 /* MPOL_BIND */, mask, 1024, 0);  // best effort
+    if (cudaHostRegister(p, bytes, cudaHostRegisterPortable | cudaHostRegisterMapped) != cudaSuccess) {
+        cudaGetLastError();
+        munmap(p, bytes);
+        return nullptr;
+    }
+    *registered = true;
+    return p;
+}
+
 }  // namespace
 
 enum class State { IDLE, ACTIVE, DRAINING, READY, ABORTED };
@@ -127,6 +187,9 @@ struct gck_ctx {
     // pinned host arena
     char *arena = nullptr;
     char *arena_dev = nullptr;  // device view of the mapped arena (zero-copy drain)
+    bool arena_registered = false;  // mmap + cudaHostRegister (NUMA-bound) vs cudaHostAlloc
+    int numa = -1;                  // node the arena / host threads are bound to
+    cpu_set_t numa_cpus;            // that node's CPUs
     uint64_t arena_bytes = 0;
     float *h_master = nullptr, *h_m = nullptr, *h_v = nullptr;
     uint16_t *h_glog = nullptr;   // base of the gradient log
@@ -232,7 +295,7 @@ struct gck_ctx {
                 for (uint32_t i = 0; i < K; ++i) gl[i] = glog[i];
                 const auto r0 = std::chrono::steady_clock::now();
                 st = gck::replay_host_impl(recs, K, lo, hi, h_master, h_m, h_v, gl, cfg.replay_threads,
-                                           &replay_threads_used);
+                                           &replay_threads_used, numa >= 0 ? &numa_cpus : nullptr);
                 replay_compute_ms =
                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - r0).count();
                 replayed = (st == GCK_OK);
@@ -482,7 +545,15 @@ gck_status gck_create(const gck_config *cfg_in, const gck_hparams *hp, const gck
     }
     const uint64_t sec = align_up(cfg.n * 4, kAlign);
     c->arena_bytes = 3 * sec + glog_max * 2;
-    e = cudaHostAlloc((void **)&c->arena, c->arena_bytes, cudaHostAllocPortable | cudaHostAllocMapped);
+    c->numa = cfg.numa_node >= 0 ? cfg.numa_node : (cfg.numa_node == -1 ? gpu_numa_node(cfg.device) : -1);
+    if (c->numa >= 0 && !node_cpus(c->numa, &c->numa_cpus)) c->numa = -1;
+    if (c->numa >= 0) {
+        c->arena = static_cast<char *>(alloc_pinned_on_node(c->arena_bytes, c->numa, &c->arena_registered));
+        e = c->arena ? cudaSuccess : cudaErrorMemoryAllocation;
+    } else {
+        e = cudaHostAlloc((void **)&c->arena, c->arena_bytes, cudaHostAllocPortable | cudaHostAllocMapped);
+    }
+    c->stats.numa_node = c->numa;
     if (e != cudaSuccess) {
         cudaGetLastError();
         cudaFree(c->ring);
@@ -521,7 +592,8 @@ gck_status gck_create(const gck_config *cfg_in, const gck_hparams *hp, const gck
         gck_destroy(c);
         return set_tls(GCK_E_CUDA, "stream/event creation failed");
     }
-    c->stats.replay_threads = cfg.replay_threads > 0 ? cfg.replay_threads : gck::default_threads();
+    c->stats.replay_threads = cfg.replay_threads > 0 ? cfg.replay_threads
+                              : (c->numa >= 0 ? CPU_COUNT(&c->numa_cpus) : gck::default_threads());
     *out = c;
     return GCK_OK;
 }
@@ -546,7 +618,12 @@ gck_status gck_destroy(gck_ctx *c) {
             if (ev) cudaEventDestroy(ev);
         if (c->d2h) cudaStreamDestroy(c->d2h);
         if (c->ring) cudaFree(c->ring);
-        if (c->arena) cudaFreeHost(c->arena);
+        if (c->arena && c->arena_registered) {
+            cudaHostUnregister(c->arena);
+            munmap(c->arena, c->arena_bytes);
+        } else if (c->arena) {
+            cudaFreeHost(c->arena);
+        }
     }
     delete c;
     return GCK_OK;
@@ -1067,6 +1144,7 @@ gck_status gck_persist_begin(gck_ctx *c, const char *path, uint32_t rank, uint32
     c->persist_error.clear();
     c->persist_started = true;
     c->persist_worker = std::thread([c, h, p, meta]() {
+        if (c->numa >= 0) pthread_setaffinity_np(pthread_self(), sizeof(cpu_set_t), &c->numa_cpus);
         const float *sec[3] = {c->h_master, c->h_m, c->h_v};
         std::string err;
         gck_persist_stats ps{};

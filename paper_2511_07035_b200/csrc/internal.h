@@ -2,6 +2,8 @@
 // replay (replay_host.cpp) and the sm_100a kernels (kernels.cu). Not part of the ABI.
 #pragma once
 
+#include <sched.h>
+
 #include <cstddef>
 #include <cstdint>
 #include <string>
@@ -60,7 +62,7 @@ gck_status load_checkpoint_impl(const char *path, float *const dst[3], uint64_t 
 // Host replay (replay_host.cpp).
 gck_status replay_host_impl(const gck_step_record *recs, uint32_t K, const uint64_t *lo, const uint64_t *hi,
                             float *p, float *m, float *v, const uint16_t *const *glog, int threads,
-                            int *threads_used);
+                            int *threads_used, const cpu_set_t *cpus = nullptr);
 int default_threads();
 
 }  // namespace gck

@@ -83,7 +83,7 @@ int default_threads() {
 
 gck_status replay_host_impl(const gck_step_record *recs, uint32_t K, const uint64_t *lo, const uint64_t *hi,
                             float *p, float *m, float *v, const uint16_t *const *glog, int threads,
-                            int *threads_used) {
+                            int *threads_used, const cpu_set_t *cpus) {
     if (K <= 1) {
         if (threads_used) *threads_used = 0;
         return GCK_OK;
@@ -97,11 +97,12 @@ gck_status replay_host_impl(const gck_step_record *recs, uint32_t K, const uint6
     for (uint32_t j = 0; j + 1 < K; ++j)
         for (uint64_t a = lo[j]; a < hi[j]; a += kTask) tasks.push_back(Task{j, a, std::min(hi[j], a + kTask)});
     std::stable_sort(tasks.begin(), tasks.end(), [](const Task &x, const Task &y) { return x.j < y.j; });
-    if (threads <= 0) threads = default_threads();
+    if (threads <= 0) threads = cpus ? std::max(1, CPU_COUNT(cpus)) : default_threads();
     threads = (int)std::min<uint64_t>((uint64_t)threads, std::max<uint64_t>(1, tasks.size()));
     if (threads_used) *threads_used = threads;
     std::atomic<uint64_t> next{0};
     auto worker = [&]() {
+        if (cpus) pthread_setaffinity_np(pthread_self(), sizeof(cpu_set_t), cpus);  // NUMA-local
         const unsigned saved_csr = _mm_getcsr();
         clear_ftz_daz();
         for (;;) {
@@ -118,7 +119,7 @@ gck_status replay_host_impl(const gck_step_record *recs, uint32_t K, const uint6
         }
         _mm_setcsr(saved_csr);
     };
-    if (threads == 1) {
+    if (threads == 1 && !cpus) {
         worker();
     } else {
         std::vector<std::thread> pool;

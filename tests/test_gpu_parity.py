@@ -440,3 +440,26 @@ def test_drain_failure_aborts_checkpoint_not_training(G, staging):
     assert_state_equal((ck.master, ck.exp_avg, ck.exp_avg_sq), traj[2 * K - 1], "session after the abort vs oracle")
     ctx.release()
     ctx.close()
+
+
+@pytest.mark.parametrize("numa", [0, -1, -2])
+def test_numa_bound_arena_session(G, numa):
+    """The pinned arena from mmap + mbind + cudaHostRegister on an explicit node (0), the GPU's own
+    node (-1; unbound when the platform reports none), or cudaHostAlloc (-2): same bytes out."""
+    n, K, t0 = 1 << 20, 4, 10
+    state, grads, recs, sargs = session_inputs(17, n, K, t0)
+    ctx, (p, m, v, out) = _make_ctx(G, state, K, numa_node=numa)
+    ctx.begin_checkpoint(t0, K)
+    for i in range(1, K + 1):
+        a = sargs[i - 1]
+        ctx.submit(i, a["step"], a["adam_t"], a["lr"], up_u16(grads[i - 1]), a["grad_scale"], a["skip"])
+    ck = ctx.finalize()
+    want = oracle.trajectory(*state, grads[:K - 1], recs[:K - 1])[-1]
+    assert_state_equal((ck.master, ck.exp_avg, ck.exp_avg_sq), want, f"numa {numa}")
+    st = ctx.stats()
+    if numa == 0:
+        assert st["numa_node"] == 0
+    if numa == -2:
+        assert st["numa_node"] == -1
+    ctx.release()
+    ctx.close()
