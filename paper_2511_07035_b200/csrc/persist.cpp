@@ -162,7 +162,7 @@ gck_status write_checkpoint_impl(const char *path, const gck_file_header *hdr_in
     }
     std::vector<uint32_t> table(3 * L.nblocks, 0);
     const uint64_t total = 3 * L.nblocks;
-    std::atomic<uint64_t> next{0}, done_blocks{0};
+    std::atomic<uint64_t> next{0};
     std::atomic<bool> failed{false};
     const long fault = fault_after_blocks();
     auto worker = [&]() {
@@ -179,7 +179,6 @@ gck_status write_checkpoint_impl(const char *path, const gck_file_header *hdr_in
             const char *src = reinterpret_cast<const char *>(sec[s]) + off;
             table[j] = crc32_of(src, len);
             if (!pwrite_all(fd, src, len, L.sec_off[s] + off)) failed = true;
-            done_blocks++;
         }
     };
     if (threads <= 0) threads = std::min(16, default_threads());
