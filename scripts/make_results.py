@@ -46,7 +46,7 @@ to the GPU's own synchronous snapshot over all elements and to the oracle on sam
 """ + "\n".join(row("C4 Llama-2 13B, one rank of 8 (n_r=1.63G), 2048 tok", "1 (rank of 8)", x["config"]["K"], x)
                 for x in q) + f"""
 
-(C3/C4 rows were measured before the last kernel revision: ~85% HBM at ~1.36–1.40 GHz there.)
+(C3/C4 rows: the final kernel at the power-capped ~1.35–1.40 GHz these GEMM-heavy steps run at.)
 
 - **Headline (bench.py default, C2):** {d['value']:.0f} tokens/s with a consistent checkpoint every 50
   steps vs {d['ckpt_free']['value']:.0f} checkpoint-free (ratio {d['ckpt_free']['throughput_ratio']:.4f}) at
