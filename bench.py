@@ -72,6 +72,8 @@ def parse():
                     help="NEXT-3 baselines in the same harness: sync = blocking D2H snapshot of the full "
                          "state (DeepSpeed/Async snapshot phase); async-o = the snapshot overlaps the next "
                          "step's F/B and its update waits for it (P:312-318)")
+    ap.add_argument("--replay-mode", default="host", choices=["host", "gpu"],
+                    help="consistency replay on the host pool (default) or in the GPU replay kernel")
     ap.add_argument("--replay-threads", type=int, default=0,
                     help="host replay / persist threads (0 = the host's cores divided by the local ranks)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -223,7 +225,7 @@ def main():
     fb.capture()
     ctx = G.GoCkpt(master, exp_avg, exp_avg_sq, param, **HP, k_min=K, k_max=K, part_align=1024,
                    ring_slots=args.ring_slots, copy_mode=args.copy_mode, replay_threads=args.replay_threads,
-                   timing=True, eager_replay=True, staging=args.staging)
+                   timing=True, eager_replay=True, staging=args.staging, replay_mode=args.replay_mode)
     baseline = args.scheme != "gockpt"
     if baseline:
         snap_host = [torch.empty(n, dtype=torch.float32, pin_memory=True) for _ in range(3)]
@@ -420,6 +422,7 @@ def main():
                    "fb_standin": f"{args.model} fwd+bwd GEMM chain (cuBLAS bf16, CUDA graph)",
                    "fb_tflop_per_step": fb.flops / 1e12, "copy_mode": args.copy_mode,
                    "ring_slots": args.ring_slots, "staging": args.staging, "scheme": args.scheme,
+                   "replay_mode": args.replay_mode,
                    "parallelism": f"zero1-dp{world}",
                    "l2": f"inputs larger than L2 ({12 * n / 1e9:.2f} GB fp32 state + {2 * n / 1e9:.2f} GB gradient "
                          f"per step per rank)",

@@ -90,7 +90,10 @@ typedef struct {
                                (SM stores into mapped pinned memory) */
     uint64_t chunk_bytes;   /* copy-engine chunk size (0 = one copy per section); P:362 uses 4 MiB */
     uint32_t zc_ctas;       /* CTAs of the zero-copy drain kernel (0 -> 32) */
-    int32_t replay_mode;    /* GCK_REPLAY_HOST (thread pool) or GCK_REPLAY_GPU */
+    int32_t replay_mode;    /* GCK_REPLAY_HOST: the host thread pool replays in place;
+                               GCK_REPLAY_GPU: the stale parts + gradient log go back up to HBM, the
+                               replay kernel runs there, the consistent parts come back (no host
+                               arithmetic; library-owned device scratch allocated on first use) */
     int32_t replay_threads; /* host replay threads (0 -> all cores of the affinity mask) */
     int32_t timing;         /* 1: record CUDA events for stall / kernel / D2H times (gck_stats) */
     int32_t eager_replay;   /* 1: replay starts on a library thread as soon as the gradient log is

@@ -229,6 +229,11 @@ struct gck_ctx {
     double replay_compute_ms = 0;  // the host replay itself
     int replay_threads_used = 0;
 
+    // GPU replay mode: library-owned device scratch + stream for the staged-parts round trip
+    cudaStream_t rstream = nullptr;
+    char *rscratch = nullptr;
+    uint64_t rscratch_bytes = 0;
+
     // bias-correction count tracking (the checkpoint records the count of S(T))
     uint64_t count_known = 0;   // count after the last submitted update (0 until known)
     uint64_t ckpt_adam_t = 0;
@@ -280,6 +285,61 @@ struct gck_ctx {
         if (persist_worker.joinable()) persist_worker.join();
     }
 
+    // a5, GPU variant as the finalize path (replay_mode = GCK_REPLAY_GPU): upload the stale parts
+    // 1..K-1 and the gradient log into library-owned HBM scratch, run the replay kernel, download
+    // the consistent parts. The host CPU does no arithmetic; costs PCIe round-trip bytes instead.
+    gck_status replay_on_gpu() {
+        if (K < 2) return GCK_OK;
+        const uint64_t nr = hi[K - 2];  // parts 1..K-1 = [0, hi_{K-1})
+        const uint64_t sb = (nr * 4 + 255) / 256 * 256;
+        uint64_t need = 3 * sb, goff[GCK_K_LIMIT];
+        for (uint32_t i = 0; i + 1 < K; ++i) {
+            goff[i] = need;
+            need += (hi[i] * 2 + 255) / 256 * 256;
+        }
+        cudaError_t e = cudaSuccess;
+        if (rscratch_bytes < need) {
+            if (rscratch) cudaFree(rscratch);
+            rscratch = nullptr;
+            rscratch_bytes = 0;
+            if ((e = cudaMalloc((void **)&rscratch, need)) != cudaSuccess) return GCK_E_NOMEM;
+            rscratch_bytes = need;
+        }
+        float *dp = reinterpret_cast<float *>(rscratch), *dm = reinterpret_cast<float *>(rscratch + sb),
+              *dv = reinterpret_cast<float *>(rscratch + 2 * sb);
+        if ((e = cudaMemcpyAsync(dp, h_master, nr * 4, cudaMemcpyHostToDevice, rstream)) != cudaSuccess ||
+            (e = cudaMemcpyAsync(dm, h_m, nr * 4, cudaMemcpyHostToDevice, rstream)) != cudaSuccess ||
+            (e = cudaMemcpyAsync(dv, h_v, nr * 4, cudaMemcpyHostToDevice, rstream)) != cudaSuccess)
+            return GCK_E_ABORTED;
+        gck::ReplayArgs ra;
+        std::memset(&ra, 0, sizeof(ra));
+        ra.p = dp;
+        ra.m = dm;
+        ra.v = dv;
+        ra.K = K;
+        ra.n_replay = nr;
+        for (uint32_t i = 0; i < K; ++i) {
+            ra.lo[i] = lo[i];
+            ra.hi[i] = hi[i];
+            ra.rec[i] = recs[i];
+            if (i + 1 < K) {
+                uint16_t *dg = reinterpret_cast<uint16_t *>(rscratch + goff[i]);
+                if (cudaMemcpyAsync(dg, glog[i], hi[i] * 2, cudaMemcpyHostToDevice, rstream) != cudaSuccess)
+                    return GCK_E_ABORTED;
+                ra.glog[i] = dg;
+            }
+        }
+        if (gck::launch_replay(ra, rstream, num_sms)) return GCK_E_ABORTED;
+        stats.gpu_launches++;
+        if ((e = cudaMemcpyAsync(h_master, dp, nr * 4, cudaMemcpyDeviceToHost, rstream)) != cudaSuccess ||
+            (e = cudaMemcpyAsync(h_m, dm, nr * 4, cudaMemcpyDeviceToHost, rstream)) != cudaSuccess ||
+            (e = cudaMemcpyAsync(h_v, dv, nr * 4, cudaMemcpyDeviceToHost, rstream)) != cudaSuccess ||
+            (e = cudaStreamSynchronize(rstream)) != cudaSuccess)
+            return GCK_E_ABORTED;
+        replay_threads_used = 0;
+        return GCK_OK;
+    }
+
     // Runs on the worker thread (eager) or inside finalize.
     void run_replay() {
         const auto t_start = std::chrono::steady_clock::now();
@@ -294,8 +354,11 @@ struct gck_ctx {
                 const uint16_t *gl[GCK_K_LIMIT];
                 for (uint32_t i = 0; i < K; ++i) gl[i] = glog[i];
                 const auto r0 = std::chrono::steady_clock::now();
-                st = gck::replay_host_impl(recs, K, lo, hi, h_master, h_m, h_v, gl, cfg.replay_threads,
-                                           &replay_threads_used, numa >= 0 ? &numa_cpus : nullptr);
+                if (cfg.replay_mode == GCK_REPLAY_GPU)
+                    st = replay_on_gpu();
+                else
+                    st = gck::replay_host_impl(recs, K, lo, hi, h_master, h_m, h_v, gl, cfg.replay_threads,
+                                               &replay_threads_used, numa >= 0 ? &numa_cpus : nullptr);
                 replay_compute_ms =
                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - r0).count();
                 replayed = (st == GCK_OK);
@@ -495,7 +558,8 @@ gck_status gck_create(const gck_config *cfg_in, const gck_hparams *hp, const gck
         return set_tls(GCK_E_INVALID, "bad staging");
     if (cfg.copy_mode != GCK_COPY_ENGINE && cfg.copy_mode != GCK_COPY_ZEROCOPY)
         return set_tls(GCK_E_INVALID, "bad copy_mode");
-    if (cfg.replay_mode != GCK_REPLAY_HOST) return set_tls(GCK_E_INVALID, "replay_mode: only GCK_REPLAY_HOST at finalize (GPU replay: gck_replay_gpu)");
+    if (cfg.replay_mode != GCK_REPLAY_HOST && cfg.replay_mode != GCK_REPLAY_GPU)
+        return set_tls(GCK_E_INVALID, "bad replay_mode");
     if (!(hp->beta1 > 0 && hp->beta1 < 1 && hp->beta2 > 0 && hp->beta2 < 1 && hp->eps > 0 && hp->weight_decay >= 0))
         return set_tls(GCK_E_INVALID, "hyperparameters out of range");
     if (!t->master || !t->exp_avg || !t->exp_avg_sq) return set_tls(GCK_E_INVALID, "null state tensor");
@@ -572,6 +636,8 @@ gck_status gck_create(const gck_config *cfg_in, const gck_hparams *hp, const gck
     int least = 0, greatest = 0;
     cudaDeviceGetStreamPriorityRange(&least, &greatest);
     bool ok = cudaStreamCreateWithPriority(&c->d2h, cudaStreamNonBlocking, least) == cudaSuccess;
+    if (ok && cfg.replay_mode == GCK_REPLAY_GPU)
+        ok = cudaStreamCreateWithPriority(&c->rstream, cudaStreamNonBlocking, least) == cudaSuccess;
     for (int s = 0; s < 2 && ok; ++s) {
         ok = cudaEventCreateWithFlags(&c->packed[s], cudaEventDisableTiming) == cudaSuccess &&
              cudaEventCreateWithFlags(&c->slot_free[s], cudaEventDisableTiming) == cudaSuccess;
@@ -617,6 +683,11 @@ gck_status gck_destroy(gck_ctx *c) {
         for (cudaEvent_t ev : {c->ev_upd, c->ev_grad_src, c->ev_grad_copied})
             if (ev) cudaEventDestroy(ev);
         if (c->d2h) cudaStreamDestroy(c->d2h);
+        if (c->rstream) {
+            cudaStreamSynchronize(c->rstream);
+            cudaStreamDestroy(c->rstream);
+        }
+        if (c->rscratch) cudaFree(c->rscratch);
         if (c->ring) cudaFree(c->ring);
         if (c->arena && c->arena_registered) {
             cudaHostUnregister(c->arena);

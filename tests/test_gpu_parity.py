@@ -463,3 +463,32 @@ def test_numa_bound_arena_session(G, numa):
         assert st["numa_node"] == -1
     ctx.release()
     ctx.close()
+
+
+@pytest.mark.parametrize("n,K,staging,eager", [(1_000_003, 4, "ring", True), (1 << 20, 8, "direct", False),
+                                              (124_439_808, 8, "ring", True)])
+def test_gpu_replay_finalize_mode(G, n, K, staging, eager):
+    """replay_mode='gpu': the consistency update runs in the replay kernel (stale parts and the
+    gradient log uploaded to library scratch, consistent parts downloaded) — same bytes as the
+    host replay and the synchronous snapshot."""
+    t0, seed = 20, 8
+    dev = torch.device("cuda", 0)
+    p = torch.empty(n, dtype=torch.float32, device=dev)
+    m, v = torch.empty_like(p), torch.empty_like(p)
+    G.h_generate(1, p, seed, 0, 0, 0)
+    G.h_generate(2, m, seed)
+    G.h_generate(3, v, seed)
+    g = torch.empty(n, dtype=torch.int16, device=dev)
+    ctx = G.GoCkpt(p, m, v, None, **HP, k_min=K, k_max=K, staging=staging, eager_replay=eager, replay_mode="gpu")
+    ctx.begin_checkpoint(t0, K)
+    for i in range(1, K + 1):
+        ctx.grad_fence()
+        G.h_generate(4, g, seed, t0 + i, 0, 1, 4)
+        if i == K:
+            snap = ctx.sync_snapshot()
+        ctx.submit(i, t0 + i, t0 + i, 1e-3, g)
+    ck = ctx.finalize()
+    assert_state_equal((ck.master, ck.exp_avg, ck.exp_avg_sq), snap, "gpu-replay finalize vs snapshot")
+    assert ctx.stats()["replay_threads"] == 0
+    ctx.release()
+    ctx.close()
