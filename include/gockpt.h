@@ -120,6 +120,9 @@ typedef struct {
     float *exp_avg;         /* fp32[n] Adam m (device) */
     float *exp_avg_sq;      /* fp32[n] Adam v (device) */
     uint16_t *param_bf16;   /* bf16[n] working params written as RNE(master') (device; NULL = skip) */
+    void *ring;             /* optional caller-owned HBM staging ring (device, 256-B aligned; NULL = the
+                               library allocates it); ring staging only */
+    uint64_t ring_bytes;    /* its capacity; must be >= gck_ring_bytes_required(...) */
 } gck_tensors;
 
 /* One training step's update (§2.1: update N consumes G^N). */
@@ -179,6 +182,10 @@ typedef struct {
 } gck_stats;
 
 /* ---- context lifecycle -------------------------------------------------- */
+
+/* HBM bytes the ring needs for (n, K in [k_min, k_max], A, R slots): R x the largest
+ * 256-B-aligned [master_i | m_i | v_i | G[0:hi_i]] slot. Host-only. 0 on invalid input. */
+uint64_t gck_ring_bytes_required(uint64_t n, uint32_t k_min, uint32_t k_max, uint32_t part_align, uint32_t ring_slots);
 
 /* Validate, create the D2H stream + events, allocate the HBM staging ring
  * (R slots sized for K in [k_min, k_max]) and the pinned host arena

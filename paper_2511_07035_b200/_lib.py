@@ -44,7 +44,7 @@ class Config(C.Structure):
 
 class Tensors(C.Structure):
     _fields_ = [("master", C.c_void_p), ("exp_avg", C.c_void_p), ("exp_avg_sq", C.c_void_p),
-                ("param_bf16", C.c_void_p)]
+                ("param_bf16", C.c_void_p), ("ring", C.c_void_p), ("ring_bytes", C.c_uint64)]
 
 
 class StepArgs(C.Structure):
@@ -146,6 +146,7 @@ SIGNATURES = {
     "gck_model_stall_gockpt": (C.c_double, [C.c_uint32, C.c_double, C.c_double]),
     "gck_recommend_k": (C.c_int, [C.c_uint64, C.c_uint32, C.c_double, C.c_double, C.c_double, C.c_uint32,
                                   C.POINTER(C.c_uint32), C.POINTER(C.c_double)]),
+    "gck_ring_bytes_required": (C.c_uint64, [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32]),
     "gck_device_count": (C.c_int32, []),
 }
 

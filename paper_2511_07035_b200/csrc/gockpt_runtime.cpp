@@ -93,6 +93,23 @@ SlotLayout slot_layout(uint64_t part_elems, uint64_t grad_elems) {
     return s;
 }
 
+void ring_sizes(uint64_t n, uint32_t k_min, uint32_t k_max, uint32_t A, uint64_t *slot_max, uint64_t *glog_max) {
+    *slot_max = *glog_max = 0;
+    const uint64_t U = (n + A - 1) / A;
+    const uint32_t kmax_eff = (uint32_t)std::min<uint64_t>(k_max, U);
+    for (uint32_t K = k_min; K <= kmax_eff; ++K) {
+        uint64_t lo[GCK_K_LIMIT], hi[GCK_K_LIMIT];
+        plan_parts(n, K, A, lo, hi);
+        uint64_t gsum = 0;
+        for (uint32_t i = 0; i < K; ++i) {
+            const uint64_t ghi = (i + 1 < K) ? hi[i] : 0;
+            *slot_max = std::max(*slot_max, slot_layout(hi[i] - lo[i], ghi).bytes);
+            gsum += align_up(ghi, 128);
+        }
+        *glog_max = std::max(*glog_max, gsum);
+    }
+}
+
 void fill_record(double beta1, double beta2, double eps, double wd, double pow1, double pow2, uint64_t t,
                  double lr, double gs, int32_t skip, gck_step_record *out) {
     std::memset(out, 0, sizeof(*out));
@@ -181,6 +198,7 @@ struct gck_ctx {
 
     // HBM ring
     char *ring = nullptr;
+    bool ring_owned = true;
     uint64_t slot_bytes = 0;
     uint32_t R = 2;
 
@@ -436,6 +454,16 @@ gck_status gck_make_step_record(const gck_hparams *hp, uint64_t adam_t, double l
     return GCK_OK;
 }
 
+uint64_t gck_ring_bytes_required(uint64_t n, uint32_t k_min, uint32_t k_max, uint32_t part_align,
+                                 uint32_t ring_slots) {
+    const uint32_t A = part_align ? part_align : 1024;
+    const uint32_t R = ring_slots ? ring_slots : 2;
+    if (n == 0 || k_min == 0 || k_max < k_min || k_max > GCK_K_LIMIT || R > 2 || (A % 8)) return 0;
+    uint64_t slot = 0, glog = 0;
+    ring_sizes(n, k_min, k_max, A, &slot, &glog);
+    return slot * R;
+}
+
 gck_status gck_plan_parts(uint64_t n, uint32_t K, uint32_t A, uint64_t *lo_hi) {
     if (!lo_hi) return set_tls(GCK_E_INVALID, "null lo_hi");
     uint64_t lo[GCK_K_LIMIT], hi[GCK_K_LIMIT];
@@ -585,23 +613,23 @@ gck_status gck_create(const gck_config *cfg_in, const gck_hparams *hp, const gck
 
     // sizes: worst case over K in [k_min, min(k_max, U)]
     uint64_t slot_max = 0, glog_max = 0;
-    const uint32_t kmax_eff = (uint32_t)std::min<uint64_t>(cfg.k_max, U);
-    for (uint32_t K = cfg.k_min; K <= kmax_eff; ++K) {
-        uint64_t lo[GCK_K_LIMIT], hi[GCK_K_LIMIT];
-        plan_parts(cfg.n, K, cfg.part_align, lo, hi);
-        uint64_t gsum = 0;
-        for (uint32_t i = 0; i < K; ++i) {
-            const uint64_t ghi = (i + 1 < K) ? hi[i] : 0;
-            slot_max = std::max(slot_max, slot_layout(hi[i] - lo[i], ghi).bytes);
-            gsum += align_up(ghi, 128);
-        }
-        glog_max = std::max(glog_max, gsum);
-    }
+    ring_sizes(cfg.n, cfg.k_min, cfg.k_max, cfg.part_align, &slot_max, &glog_max);
     c->direct = (cfg.staging == GCK_STAGE_DIRECT || cfg.staging == GCK_STAGE_BLOCKING);
     c->blocking_grad = (cfg.staging == GCK_STAGE_BLOCKING);
     c->slot_bytes = c->direct ? 0 : slot_max;
     c->glog_elems_cap = glog_max;
-    cudaError_t e = c->direct ? cudaSuccess : cudaMalloc((void **)&c->ring, c->slot_bytes * c->R);
+    cudaError_t e = cudaSuccess;
+    if (!c->direct && t->ring) {  // caller-owned ring (e.g. from the PyTorch caching allocator)
+        if (t->ring_bytes < c->slot_bytes * c->R || (reinterpret_cast<uintptr_t>(t->ring) & 255u)) {
+            delete c;
+            return set_tls(GCK_E_INVALID, "caller ring too small or not 256-byte aligned");
+        }
+        c->ring = static_cast<char *>(t->ring);
+        c->ring_owned = false;
+    } else if (!c->direct) {
+        e = cudaMalloc((void **)&c->ring, c->slot_bytes * c->R);
+        c->ring_owned = true;
+    }
     if (e != cudaSuccess) {
         cudaGetLastError();
         delete c;
@@ -620,7 +648,7 @@ gck_status gck_create(const gck_config *cfg_in, const gck_hparams *hp, const gck
     c->stats.numa_node = c->numa;
     if (e != cudaSuccess) {
         cudaGetLastError();
-        cudaFree(c->ring);
+        if (c->ring_owned && c->ring) cudaFree(c->ring);
         delete c;
         return set_tls(GCK_E_NOMEM, "pinned host arena allocation failed");
     }
@@ -688,7 +716,7 @@ gck_status gck_destroy(gck_ctx *c) {
             cudaStreamDestroy(c->rstream);
         }
         if (c->rscratch) cudaFree(c->rscratch);
-        if (c->ring) cudaFree(c->ring);
+        if (c->ring && c->ring_owned) cudaFree(c->ring);
         if (c->arena && c->arena_registered) {
             cudaHostUnregister(c->arena);
             munmap(c->arena, c->arena_bytes);

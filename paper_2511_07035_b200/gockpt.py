@@ -164,6 +164,10 @@ def h_generate(kind, out, seed, step=0, offset=0, mode=0, zero_per_256=4, stream
                                _stream_ptr(stream)))
 
 
+def ring_bytes_required(n: int, k_min: int, k_max: int, part_align: int = 1024, ring_slots: int = 2) -> int:
+    return int(lib().gck_ring_bytes_required(n, k_min, k_max, part_align, ring_slots))
+
+
 def device_count() -> int:
     return int(lib().gck_device_count())
 
@@ -183,7 +187,7 @@ class GoCkpt:
     def __init__(self, master, exp_avg, exp_avg_sq, param_bf16=None, *, beta1=0.9, beta2=0.999, eps=1e-8,
                  weight_decay=0.01, k_min=1, k_max=8, part_align=1024, ring_slots=2, copy_mode="ce",
                  chunk_bytes=0, zc_ctas=0, replay_threads=0, timing=True, eager_replay=True, staging="ring",
-                 numa_node=-1, replay_mode="host"):
+                 numa_node=-1, replay_mode="host", ring=None):
         n = master.numel()
         if exp_avg.numel() != n or exp_avg_sq.numel() != n or (param_bf16 is not None and param_bf16.numel() != n):
             raise ValueError("state tensors must have the same number of elements")
@@ -197,7 +201,10 @@ class GoCkpt:
                        numa_node)
         hp = L.Hparams(beta1, beta2, eps, weight_decay)
         self.hparams = dict(beta1=beta1, beta2=beta2, eps=eps, weight_decay=weight_decay)
-        t = L.Tensors(_dptr(master), _dptr(exp_avg), _dptr(exp_avg_sq), _dptr(param_bf16))
+        # ring: an optional caller-owned uint8 CUDA tensor of >= ring_bytes_required(...) bytes
+        t = L.Tensors(_dptr(master), _dptr(exp_avg), _dptr(exp_avg_sq), _dptr(param_bf16), _dptr(ring),
+                      ring.numel() * ring.element_size() if ring is not None else 0)
+        self._ring = ring
         ctx = C.c_void_p()
         check(lib().gck_create(C.byref(cfg), C.byref(hp), C.byref(t), C.byref(ctx)))
         self._ctx = ctx

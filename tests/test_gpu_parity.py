@@ -492,3 +492,28 @@ def test_gpu_replay_finalize_mode(G, n, K, staging, eager):
     assert ctx.stats()["replay_threads"] == 0
     ctx.release()
     ctx.close()
+
+
+def test_caller_owned_ring(G):
+    """SURVEY §8(b) ownership: PyTorch may own the HBM ring (caching-allocator accounting)."""
+    from paper_2511_07035_b200 import GckError
+    from paper_2511_07035_b200 import _lib as L
+    n, K, t0 = 1_000_003, 4, 10
+    state, grads, recs, sargs = session_inputs(23, n, K, t0)
+    need = G.ring_bytes_required(n, K, K, 1024, 2)
+    p, m, v = (up_f32(x) for x in state)
+    with pytest.raises(GckError) as e:
+        G.GoCkpt(p, m, v, None, **HP, k_min=K, k_max=K, ring=torch.empty(need - 256, dtype=torch.uint8, device="cuda"))
+    assert e.value.status == L.E_INVALID
+    ring = torch.empty(need, dtype=torch.uint8, device="cuda")
+    ctx = G.GoCkpt(p, m, v, None, **HP, k_min=K, k_max=K, ring=ring)
+    ctx.begin_checkpoint(t0, K)
+    for i in range(1, K + 1):
+        a = sargs[i - 1]
+        ctx.submit(i, a["step"], a["adam_t"], a["lr"], up_u16(grads[i - 1]), a["grad_scale"], a["skip"])
+    ck = ctx.finalize()
+    want = oracle.trajectory(*state, grads[:K - 1], recs[:K - 1])[-1]
+    assert_state_equal((ck.master, ck.exp_avg, ck.exp_avg_sq), want, "caller-owned ring")
+    ctx.release()
+    ctx.close()
+    del ring                                   # freed by torch, not by the library

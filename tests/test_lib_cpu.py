@@ -225,3 +225,16 @@ def test_replay_host_rejects_bad_parts(G):
     for parts in ([(0, 5), (6, 10)], [(0, 5), (5, 9)], [(1, 5), (5, 10)], [(0, 5), (5, 5)]):
         with pytest.raises(GckError):
             G.replay_host(recs, parts, p, p.copy(), p.copy(), g)
+
+
+def test_ring_bytes_required(G):
+    # R x the largest 256-B-aligned [master_i | m_i | v_i | G[0:hi_i]] slot over K in [k_min, k_max]
+    al = lambda x: (x + 255) // 256 * 256
+    for n, kmin, kmax, A, R in [(124_439_808, 8, 8, 1024, 2), (1 << 20, 2, 8, 1024, 1), (1000, 1, 4, 8, 2)]:
+        best = 0
+        for K in range(kmin, kmax + 1):
+            parts = oracle.make_parts(n, K, A)
+            for i, (lo, hi) in enumerate(parts):
+                best = max(best, 3 * al(4 * (hi - lo)) + al(2 * (hi if i < K - 1 else 0)))
+        assert G.ring_bytes_required(n, kmin, kmax, A, R) == R * best
+    assert G.ring_bytes_required(0, 1, 4) == 0 and G.ring_bytes_required(100, 5, 4) == 0
