@@ -404,6 +404,9 @@ def main():
                          f"{dt:.1f} s measured, time scaled x{n / n_s:.1f}; AdamW + capture + replay only, no F/B"}
 
     sess_stall_delta = [max(0.0, t - free_med) for t in sess_ms]
+    # NEXT-4: the analytic model's K for this step time and link (smallest K whose largest per-step
+    # transfer fits in one step), next to the K this run used
+    k_rec, vmax_rec = G.recommend_k(n, link_peak, free_med / 1e3, 1.0, 64)
     line = {
         "metric": METRIC,
         "value": value,
@@ -441,6 +444,8 @@ def main():
                 "link_peak_gbs": link_peak, "frac": (d2h_bytes / (d2h_ms / 1e3) / 1e9) / link_peak if d2h_ms else None,
                 "bytes_per_session": session_bytes, "link_peak_how": "best of 5 x 1 GiB cudaMemcpyAsync D2H "
                 "into pinned memory, this run"},
+        "model": {"recommended_K": k_rec, "v_max_bytes_at_recommended_K": vmax_rec, "K_used": K,
+                  "note": "gck_recommend_k(n, measured link GB/s, checkpoint-free step time)"},
         "replay": {"host_ms_last_session": st1["last_replay_ms"], "threads": st1["replay_threads"],
                    "worker_ms_last_session": st1["last_worker_ms"],
                    "finalize_wait_ms_last": st1["last_finalize_wait_ms"],
