@@ -340,6 +340,13 @@ gck_status gck_read_header(const char *path, gck_file_header *out);
 gck_status gck_load_checkpoint(const char *path, uint64_t n, float *master, float *m, float *v, int32_t threads,
                                gck_file_header *out, gck_persist_stats *stats);
 
+/* Read elements [offset, offset + count) of a checkpoint file's master / m / v into host arrays of
+ * count floats; every 64 MiB block the range touches is read whole and CRC-verified. For loading
+ * into a different ZeRO-1 degree: a new rank's range spans parts of old ranks' files.
+ * Host-only. Errors: INVALID (range outside n), IO, CORRUPT. */
+gck_status gck_load_checkpoint_range(const char *path, uint64_t offset, uint64_t count, float *master, float *m,
+                                     float *v, int32_t threads, gck_file_header *out);
+
 /* Persist the finalized checkpoint (state READY) in the background on a library thread;
  * gck_release (and gck_destroy) wait for it, so the next session cannot begin before the
  * previous checkpoint is durable ("GoCkpt will wait for the last checkpoint"). */

@@ -136,6 +136,8 @@ SIGNATURES = {
     "gck_read_header": (C.c_int, [C.c_char_p, C.POINTER(FileHeader)]),
     "gck_load_checkpoint": (C.c_int, [C.c_char_p, C.c_uint64, P, P, P, C.c_int32, C.POINTER(FileHeader),
                                       C.POINTER(PersistStats)]),
+    "gck_load_checkpoint_range": (C.c_int, [C.c_char_p, C.c_uint64, C.c_uint64, P, P, P, C.c_int32,
+                                            C.POINTER(FileHeader)]),
     "gck_persist_begin": (C.c_int, [P, C.c_char_p, C.c_uint32, C.c_uint32, C.c_char_p]),
     "gck_persist_wait": (C.c_int, [P, C.POINTER(PersistStats)]),
     "gck_restore": (C.c_int, [P, C.c_char_p, P, C.POINTER(FileHeader)]),

@@ -1223,6 +1223,15 @@ gck_status gck_load_checkpoint(const char *path, uint64_t n, float *master, floa
     return st == GCK_OK ? st : set_tls(st, err);
 }
 
+gck_status gck_load_checkpoint_range(const char *path, uint64_t offset, uint64_t count, float *master, float *m,
+                                     float *v, int32_t threads, gck_file_header *out) {
+    if (!path || (count && (!master || !m || !v))) return set_tls(GCK_E_INVALID, "null argument");
+    float *dst[3] = {master, m, v};
+    std::string err;
+    const gck_status st = gck::load_range_impl(path, offset, count, dst, threads, out, &err);
+    return st == GCK_OK ? st : set_tls(st, err);
+}
+
 gck_status gck_persist_begin(gck_ctx *c, const char *path, uint32_t rank, uint32_t world, const char *meta_json) {
     if (!c || !path) return set_tls(GCK_E_INVALID, "null argument");
     if (c->state != State::READY) return c->fail(GCK_E_PROTOCOL, "persist needs a finalized, unreleased checkpoint");

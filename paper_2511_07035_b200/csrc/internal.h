@@ -59,6 +59,9 @@ gck_status read_header_impl(const char *path, gck_file_header *out, std::string 
 gck_status load_checkpoint_impl(const char *path, float *const dst[3], uint64_t n, int threads, gck_file_header *hdr_out,
                                 gck_persist_stats *stats, std::string *err);
 
+gck_status load_range_impl(const char *path, uint64_t offset, uint64_t count, float *const dst[3], int threads,
+                           gck_file_header *hdr_out, std::string *err);
+
 // Host replay (replay_host.cpp).
 gck_status replay_host_impl(const gck_step_record *recs, uint32_t K, const uint64_t *lo, const uint64_t *hi,
                             float *p, float *m, float *v, const uint16_t *const *glog, int threads,

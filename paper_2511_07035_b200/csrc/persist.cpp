@@ -354,4 +354,74 @@ gck_status load_checkpoint_impl(const char *path, float *const dst[3], uint64_t 
     return GCK_OK;
 }
 
+// Elements [offset, offset + count) of a checkpoint file's three sections, every touched block
+// read whole and CRC-verified (resharding on load: a new ZeRO-1 rank's range spans parts of old
+// ranks' files; "during loading, these shards are fetched").
+gck_status load_range_impl(const char *path, uint64_t offset, uint64_t count, float *const dst[3], int threads,
+                           gck_file_header *hdr_out, std::string *err) {
+    gck_file_header h;
+    gck_status st = read_header_impl(path, &h, err);
+    if (st != GCK_OK) return st;
+    if (offset > h.n || count > h.n - offset) {
+        *err = "range [" + std::to_string(offset) + ", +" + std::to_string(count) + ") outside n = " + std::to_string(h.n);
+        return GCK_E_INVALID;
+    }
+    const Layout L = layout_for(h.n);
+    if (h.nblocks != L.nblocks || h.table_offset != L.table_off) {
+        *err = "layout fields inconsistent with n";
+        return GCK_E_CORRUPT;
+    }
+    if (hdr_out) *hdr_out = h;
+    if (count == 0) return GCK_OK;
+    const int fd = ::open(path, O_RDONLY);
+    if (fd < 0) {
+        *err = std::string("open: ") + strerror(errno);
+        return GCK_E_IO;
+    }
+    std::vector<uint32_t> table(3 * L.nblocks);
+    if (!pread_all(fd, table.data(), table.size() * 4, L.table_off) ||
+        crc32_of(table.data(), table.size() * 4) != h.table_crc) {
+        ::close(fd);
+        *err = "CRC table unreadable or corrupt";
+        return GCK_E_CORRUPT;
+    }
+    const uint64_t b0 = offset * 4 / kBlock, b1 = ((offset + count) * 4 + kBlock - 1) / kBlock;
+    const uint64_t nb = b1 - b0, total = 3 * nb;
+    std::atomic<uint64_t> next{0};
+    std::atomic<int> bad{0};
+    auto worker = [&]() {
+        std::vector<char> buf;
+        for (;;) {
+            const uint64_t j = next.fetch_add(1);
+            if (j >= total || bad.load()) break;
+            const int s = (int)(j / nb);
+            const uint64_t b = b0 + j % nb;
+            const uint64_t off = b * kBlock, len = std::min(kBlock, L.sec_bytes - off);
+            buf.resize(len);
+            if (!pread_all(fd, buf.data(), len, L.sec_off[s] + off)) {
+                bad = 1;
+                break;
+            }
+            if (crc32_of(buf.data(), len) != table[s * L.nblocks + b]) {
+                bad = 2;
+                break;
+            }
+            const uint64_t lo = std::max(off, offset * 4), hi = std::min(off + len, (offset + count) * 4);
+            std::memcpy(reinterpret_cast<char *>(dst[s]) + (lo - offset * 4), buf.data() + (lo - off), hi - lo);
+        }
+    };
+    if (threads <= 0) threads = std::min(16, default_threads());
+    threads = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)threads, total));
+    std::vector<std::thread> pool;
+    for (int k = 1; k < threads; ++k) pool.emplace_back(worker);
+    worker();
+    for (auto &t : pool) t.join();
+    ::close(fd);
+    if (bad) {
+        *err = bad == 1 ? "truncated or unreadable data section" : "data CRC mismatch in a touched block";
+        return GCK_E_CORRUPT;
+    }
+    return GCK_OK;
+}
+
 }  // namespace gck

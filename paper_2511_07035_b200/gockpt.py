@@ -146,6 +146,16 @@ def load_checkpoint(path: str, n: int, threads: int = 0):
     return out[0], out[1], out[2], _hdr_dict(h), st.as_dict()
 
 
+def load_checkpoint_range(path: str, offset: int, count: int, out=None, threads: int = 0):
+    """gck_load_checkpoint_range -> (master, m, v) numpy views of `out` (3 x count float32) + header."""
+    if out is None:
+        out = [np.empty(count, np.float32) for _ in range(3)]
+    h = L.FileHeader()
+    check(lib().gck_load_checkpoint_range(path.encode(), offset, count, *[o.ctypes.data for o in out], threads,
+                                          C.byref(h)))
+    return out[0], out[1], out[2], _hdr_dict(h)
+
+
 def recommend_k(n: int, link_gbs: float, t_step_s: float, budget: float = 1.0, k_max: int = 16, A: int = 1024):
     """NEXT-4 (gck_recommend_k) -> (K, V_max bytes); K = 0 if none fits."""
     k, vmax = C.c_uint32(0), C.c_double(0)

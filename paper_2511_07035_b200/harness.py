@@ -207,7 +207,8 @@ def zero1_shard(n_total: int, world: int, rank: int, align: int = 1024):
     return rank * n_r, n_r, padded
 
 
-def commit_global(directory: str, step: int, local_ok: bool, files: list[str] | None = None) -> bool:
+def commit_global(directory: str, step: int, local_ok: bool, files: list[str] | None = None,
+                  n_total: int | None = None, n_per_rank: int | None = None, align: int | None = None) -> bool:
     """Global checkpoint commit ("Rank 0 monitoring completion by other Ranks"): every rank
     reports whether its shard's file is durable; rank 0 writes MANIFEST.json (atomic rename) only
     if all did. Returns whether the global checkpoint is complete."""
@@ -218,7 +219,8 @@ def commit_global(directory: str, step: int, local_ok: bool, files: list[str] | 
     rank = dist.get_rank() if dist.is_available() and dist.is_initialized() else 0
     if ok and rank == 0:
         man = {"step": step, "world": world,
-               "files": files or [f"ckpt_{step}.rank{r}.bin" for r in range(world)]}
+               "files": files or [f"ckpt_{step}.rank{r}.bin" for r in range(world)],
+               "n_total": n_total, "n_per_rank": n_per_rank, "align": align}
         tmp = os.path.join(directory, "MANIFEST.json.tmp")
         with open(tmp, "w") as fh:
             json.dump(man, fh)
@@ -226,3 +228,30 @@ def commit_global(directory: str, step: int, local_ok: bool, files: list[str] | 
             os.fsync(fh.fileno())
         os.replace(tmp, os.path.join(directory, "MANIFEST.json"))
     return ok
+
+
+def load_resharded(directory: str, world_new: int, rank_new: int, align: int | None = None):
+    """Load rank `rank_new`'s ZeRO-1 shard for a new data-parallel degree `world_new` from a global
+    checkpoint written at another degree (MANIFEST.json): the new rank's range [r'n', (r'+1)n') of
+    the flat buffer is read from the old ranks' files with gck_load_checkpoint_range (every
+    touched block CRC-verified). P:376: "during loading, these shards are fetched". Positions past
+    the model's n_total (ZeRO padding) are zero. Returns (master, m, v, step)."""
+    import json
+    import numpy as np
+    from . import gockpt as G
+    man = json.load(open(os.path.join(directory, "MANIFEST.json")))
+    N, W, n_old = man["n_total"], man["world"], man["n_per_rank"]
+    off, n_new, _ = zero1_shard(N, world_new, rank_new, align or man.get("align") or 1024)
+    out = [np.zeros(n_new, np.float32) for _ in range(3)]
+    step = None
+    for r in range(W):
+        o0 = r * n_old
+        lo, hi = max(off, o0), min(off + n_new, o0 + n_old, N)
+        if lo >= hi:
+            continue
+        views = [x[lo - off:hi - off] for x in out]
+        _, _, _, h = G.load_checkpoint_range(os.path.join(directory, man["files"][r]), lo - o0, hi - lo, views)
+        if step is not None and h["step"] != step:
+            raise ValueError("shards of different steps in one manifest")
+        step = h["step"]
+    return out[0], out[1], out[2], step

@@ -58,7 +58,7 @@ def _worker(rank, world, port, n_total, K, t0, result_dir):
         from paper_2511_07035_b200.harness import commit_global
         path = os.path.join(result_dir, f"ckpt_{t0 + K - 1}.rank{rank}.bin")
         G.write_checkpoint(path, p, m, v, step=t0 + K - 1, adam_t=t0 + K - 1, rank=rank, world=world, threads=2)
-        assert commit_global(result_dir, t0 + K - 1, True)
+        assert commit_global(result_dir, t0 + K - 1, True, n_total=n_total, n_per_rank=n_r, align=64)
         t = max_over_ranks(float(rank + 1))
         assert t == float(world)
         assert all_ranks_ok(True)
@@ -89,6 +89,16 @@ def test_two_ranks_shard_checkpoints_concatenate_to_global(tmp_path, n_total):
     assert man["step"] == t0 + K - 1 and man["world"] == world
     back = np.concatenate([np.stack(OF.read(str(tmp_path / f))[1:]) for f in man["files"]], axis=1)
     assert np.array_equal(back.view(np.uint32), got.view(np.uint32))
+    # load into other data-parallel degrees (resharding): the concatenation over the new ranks is S(T)
+    from paper_2511_07035_b200.harness import load_resharded
+    for w_new in (1, 3, 4):
+        parts = [load_resharded(str(tmp_path), w_new, r, align=64) for r in range(w_new)]
+        assert all(p[3] == t0 + K - 1 for p in parts)
+        cat = [np.concatenate([p[k] for p in parts])[:n_total] for k in range(3)]
+        for c, w in zip(cat, want):
+            assert np.array_equal(c.view(np.uint32), w[:n_total].view(np.uint32))
+        pad = np.concatenate([p[0] for p in parts])[n_total:]
+        assert not pad.any()                                     # ZeRO padding loads as zeros
 
 
 def test_zero1_shard_layout():

@@ -119,3 +119,32 @@ def test_crash_during_persist_keeps_previous_latest(G, tmp_path):
     proc.wait()
     assert OF.latest(str(tmp_path)) == good
     assert not os.path.exists(tmp_path / "ck_300.bin")
+
+
+def test_range_loader(G, tmp_path):
+    from paper_2511_07035_b200 import GckError
+    from paper_2511_07035_b200 import _lib as L
+    n = (64 << 20) // 4 * 2 + 12345                      # 3 blocks per section, ragged
+    p, m, v = state(n, 5)
+    path = str(tmp_path / "r.bin")
+    G.write_checkpoint(path, p, m, v, step=9, adam_t=9)
+    B = (64 << 20) // 4
+    for off, cnt in [(0, 1), (B - 3, 7), (B, B), (5, 2 * B + 100), (n - 10, 10), (0, n), (n, 0)]:
+        rp, rm, rv, h = G.load_checkpoint_range(path, off, cnt)
+        assert h["step"] == 9
+        for got, exp in zip((rp, rm, rv), (p, m, v)):
+            assert np.array_equal(got.view(np.uint32), exp[off:off + cnt].view(np.uint32)), (off, cnt)
+    with pytest.raises(GckError) as e:
+        G.load_checkpoint_range(path, n - 5, 6)
+    assert e.value.status == L.E_INVALID
+    # corruption in a block the range touches is detected; in an untouched block it is not read
+    _, nblocks, table_off, _, offs, _ = OF.layout(n)
+    data = bytearray(open(path, "rb").read())
+    data[offs[1] + 4 * (2 * B + 50)] ^= 1                  # m, block 2
+    bad = str(tmp_path / "bad.bin")
+    open(bad, "wb").write(bytes(data))
+    with pytest.raises(GckError) as e:
+        G.load_checkpoint_range(bad, 2 * B + 10, 100)
+    assert e.value.status == L.E_CORRUPT
+    rp, rm, rv, _ = G.load_checkpoint_range(bad, 0, B)        # blocks 0 only: fine
+    assert np.array_equal(rm, m[:B])
