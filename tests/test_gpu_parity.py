@@ -517,3 +517,49 @@ def test_caller_owned_ring(G):
     ctx.release()
     ctx.close()
     del ring                                   # freed by torch, not by the library
+
+
+@pytest.mark.parametrize("skip_at", [1, 3, 4])
+def test_skip_positions(G, skip_at):
+    n, K, t0 = 100_000, 4, 40
+    state, grads, recs, sargs = session_inputs(29, n, K, t0, skips={t0 + skip_at})
+    ctx, (p, m, v, out) = _make_ctx(G, state, K, part_align=64)
+    ctx.begin_checkpoint(t0, K)
+    for i in range(1, K + 1):
+        a = sargs[i - 1]
+        ctx.submit(i, a["step"], a["adam_t"], a["lr"], up_u16(grads[i - 1]), a["grad_scale"], a["skip"])
+    ck = ctx.finalize()
+    want = oracle.trajectory(*state, grads[:K - 1], recs[:K - 1])[-1]
+    assert_state_equal((ck.master, ck.exp_avg, ck.exp_avg_sq), want, f"skip at {skip_at}")
+    torch.cuda.synchronize()
+    assert_state_equal((down_f32(p), down_f32(m), down_f32(v)), oracle.trajectory(*state, grads, recs)[-1], "live")
+    ctx.release()
+    ctx.close()
+
+
+def test_two_contexts_interleaved_and_destroy_mid_session(G):
+    """Two shards in one process with interleaved sessions (independent streams/events/arenas), and a
+    context destroyed in the middle of a session (no leak of queued work into the survivor)."""
+    n, K, t0 = 200_003, 4, 10
+    sa = session_inputs(31, n, K, t0)
+    sb = session_inputs(37, n, K, t0)
+    ca, _ = _make_ctx(G, sa[0], K, part_align=64)
+    cb, _ = _make_ctx(G, sb[0], K, part_align=64, staging="direct")
+    cc, _ = _make_ctx(G, sa[0], K, part_align=64)
+    for c in (ca, cb, cc):
+        c.begin_checkpoint(t0, K)
+    for i in range(1, K + 1):
+        for c, (state, grads, recs, sargs) in ((ca, sa), (cb, sb), (cc, sa)):
+            if c is cc and i >= 3:
+                continue
+            a = sargs[i - 1]
+            c.grad_fence()
+            c.submit(i, a["step"], a["adam_t"], a["lr"], up_u16(grads[i - 1]), a["grad_scale"], a["skip"])
+        if i == 2:
+            cc.close()                      # destroyed mid-session
+    for c, (state, grads, recs, sargs) in ((ca, sa), (cb, sb)):
+        ck = c.finalize()
+        want = oracle.trajectory(*state, grads[:K - 1], recs[:K - 1])[-1]
+        assert_state_equal((ck.master, ck.exp_avg, ck.exp_avg_sq), want, "interleaved")
+        c.release()
+        c.close()
