@@ -287,13 +287,12 @@ __global__ void __launch_bounds__((kCW + 2) * 32, kMinBlocks) fused_adamw_pack_t
         // a dependent instruction on all loaded values makes the scoreboard wait for the LDS
         // results, __syncwarp orders the lanes before lane 0's arrive, and the proxy fence orders
         // these generic-proxy reads before the async-proxy (TMA) refill of the same bytes (WAR).
+        // (one component per LDS suffices: an LDS writes all its destination registers under one
+        // scoreboard entry, so a use of .x waits for the whole vector)
         uint32_t dep = 0;
 #pragma unroll
         for (int q = 0; q < kQ; ++q)
-            dep ^= __float_as_uint(pq[q].x) ^ __float_as_uint(pq[q].w) ^ __float_as_uint(mq[q].x) ^
-                   __float_as_uint(mq[q].w) ^ __float_as_uint(vq[q].x) ^ __float_as_uint(vq[q].w) ^ gq[q].x ^ gq[q].y ^
-                   __float_as_uint(pq[q].y) ^ __float_as_uint(pq[q].z) ^ __float_as_uint(mq[q].y) ^
-                   __float_as_uint(mq[q].z) ^ __float_as_uint(vq[q].y) ^ __float_as_uint(vq[q].z);
+            dep ^= __float_as_uint(pq[q].x) ^ __float_as_uint(mq[q].x) ^ __float_as_uint(vq[q].x) ^ gq[q].x;
         asm volatile("" : "+r"(dep));
         __syncwarp();
         if (lane == 0) {
