@@ -54,6 +54,9 @@ if rep != "-":
     open(f"profiles/{tag}_fused_adamw_pack_ncu.txt", "w").write("\n".join(lines) + "\n")
     json.dump(js, open("profiles/fused_adamw_pack_ncu.json", "w"), indent=1)
 
+print("\n".join(lines[:12]))
+if launches == "-":
+    sys.exit(0)
 rows = list(csv.reader(open(launches)))
 hi = [i for i, r in enumerate(rows) if "Kernel Name" in r][0]
 h = rows[hi]
@@ -73,5 +76,4 @@ for k, v in sorted(tot.items(), key=lambda x: -x[1]):
 gck = sum(v for k, v in tot.items() if "gck::" in k)
 L.insert(1, f"share of our kernels (gck::*): {100 * gck / T:.2f}% of GPU time")
 open(out_launches, "w").write("\n".join(L) + "\n")
-print("\n".join(lines[:12]))
 print("\n".join(L[:6]))
