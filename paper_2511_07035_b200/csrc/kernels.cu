@@ -161,6 +161,7 @@ __device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t by
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read_1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 __device__ __forceinline__ void process4(const FusedArgs &a, const RecF &r, bool skip, bool pack, uint64_t e,
@@ -228,6 +229,7 @@ __global__ void __launch_bounds__((kCW + 2) * 32, kMinBlocks) fused_adamw_pack_t
     if (warp == kCW + 1) {  // pack warp (session launches only)
         if (PACK && lane == 0) {
             uint32_t k = 0;
+            int prev_s = -1;
             for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++k) {
                 const int s = k % kStages;
                 const uint32_t ph = (k / kStages) & 1u;
@@ -250,12 +252,16 @@ __global__ void __launch_bounds__((kCW + 2) * 32, kMinBlocks) fused_adamw_pack_t
                     bulk_s2g(a.sg + base, st + kTile * 12, (uint32_t)(ghi - base) * 2);
                     issued = true;
                 }
-                if (issued) {
-                    bulk_commit();
-                    bulk_wait_read();  // the stage may be refilled only after the stores read it
-                }
-                mbar_arrive(&empty[s]);
+                // one bulk group per tile (possibly empty); keep one group's smem reads in flight
+                // while the next tile arrives, and release a stage only once its group has read it
+                bulk_commit();
+                (void)issued;
+                bulk_wait_read_1();
+                if (prev_s >= 0) mbar_arrive(&empty[prev_s]);
+                prev_s = s;
             }
+            bulk_wait_read();
+            if (prev_s >= 0) mbar_arrive(&empty[prev_s]);
             bulk_wait_all();  // slot writes complete before the CTA retires
         }
         return;
