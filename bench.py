@@ -56,7 +56,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3, help="untimed checkpoint intervals (>= 3)")
     ap.add_argument("--impl", default="gockpt", choices=["gockpt", "reference"])
     ap.add_argument("--interval", type=int, default=50)
-    ap.add_argument("--K", type=int, default=8)
+    ap.add_argument("--K", type=int, default=8,
+                    help="partitions per session; 0 = automatic (NEXT-4: chosen by the library from the measured "
+                         "step time and link during warm-up, then held for the timed region)")
     ap.add_argument("--model", default="gpt2-small", choices=list(WORKLOADS))
     ap.add_argument("--shard-of", type=int, default=0,
                     help="ZeRO-1 data-parallel degree the shard is cut for (0 = the launched world size); "
@@ -223,16 +225,16 @@ def main():
         full_param = torch.empty(n * world, dtype=torch.bfloat16, device=dev)
     fb = TransformerGemmStandIn(args.model, tokens=T, device=dev)
     fb.capture()
-    ctx = G.GoCkpt(master, exp_avg, exp_avg_sq, param, **HP, k_min=K, k_max=K, part_align=1024,
+    auto_k = K == 0
+    ctx = G.GoCkpt(master, exp_avg, exp_avg_sq, param, **HP, k_min=1 if auto_k else K, k_max=32 if auto_k else K,
+                   part_align=1024,
                    ring_slots=args.ring_slots, copy_mode=args.copy_mode, replay_threads=args.replay_threads,
                    timing=True, eager_replay=True, staging=args.staging, replay_mode=args.replay_mode)
     baseline = args.scheme != "gockpt"
     if baseline:
         snap_host = [torch.empty(n, dtype=torch.float32, pin_memory=True) for _ in range(3)]
         side = torch.cuda.Stream()
-    parts = G.plan_parts(n, K, 1024)
-    session_bytes = sum(12 * (hi - lo) + (2 * hi if i < K - 1 else 0) for i, (lo, hi) in enumerate(parts))
-    state = {"step": 0, "gen": 0}
+    state = {"step": 0, "gen": 0, "K": K if not auto_k else 32, "auto": auto_k}
 
     # ---- host-link peak: best-of-5 1 GiB D2H into pinned memory, measured in this run
     link = torch.empty(1 << 30, dtype=torch.uint8, device=dev)
@@ -304,15 +306,16 @@ def main():
 
     def interval(ckpt=True, h_grad=None, time_kernel=False, step_events=None):
         for j in range(1, I + 1):
-            part = j if (ckpt and not baseline and j <= K) else 0
-            if part == 1:
-                ctx.begin_checkpoint(state["step"], K)
+            if ckpt and not baseline and j == 1:
+                ctx.begin_checkpoint(state["step"], 0 if state["auto"] else state["K"])
+                state["K"] = ctx.stats()["last_session_k"]
+            part = j if (ckpt and not baseline and j <= state["K"]) else 0
             train_step(part, h_grad, time_kernel, step_events, snapshot=ckpt and baseline and j == 1)
         if ckpt and baseline:
             return
         if ckpt:
             ck = ctx.finalize()
-            assert ck.step == state["step"] - I + K - 1
+            assert ck.step == state["step"] - I + state["K"] - 1
             ctx.release()
             assert all_ranks_ok(True)
 
@@ -330,10 +333,14 @@ def main():
             dist.barrier()
         return max_over_ranks(e0.elapsed_time(e1) / 1e3)
 
-    # ---- warm-up (untimed)
+    # ---- warm-up (untimed); with --K 0 the library picks K here (NEXT-4) and it is then held
     for _ in range(args.warmup):
         interval(ckpt=True)
     torch.cuda.synchronize()
+    K = state["K"]
+    state["auto"] = False
+    parts = G.plan_parts(n, K, 1024)
+    session_bytes = sum(12 * (hi - lo) + (2 * hi if i < K - 1 else 0) for i, (lo, hi) in enumerate(parts))
 
     # ---- checkpoint-free reference, first half (the second half runs after the timed region, so
     #      clock/thermal drift cancels in the stall and throughput deltas)
@@ -413,6 +420,7 @@ def main():
                          f"{dt:.1f} s measured, time scaled x{n / n_s:.1f}; AdamW + capture + replay only, no F/B"}
 
     sess_stall_delta = [max(0.0, t - free_med) for t in sess_ms]
+    ctx_stats_final = ctx.stats()
     # NEXT-4: the analytic model's K for this step time and link (smallest K whose largest per-step
     # transfer fits in one step), next to the K this run used
     k_rec, vmax_rec = G.recommend_k(n, link_peak, free_med / 1e3, 1.0, 64)
@@ -455,6 +463,8 @@ def main():
                 "bytes_per_session": session_bytes, "link_peak_how": "best of 5 x 1 GiB cudaMemcpyAsync D2H "
                 "into pinned memory, this run"},
         "model": {"recommended_K": k_rec, "v_max_bytes_at_recommended_K": vmax_rec, "K_used": K,
+                  "K_automatic": auto_k, "auto_step_ms": ctx_stats_final.get("auto_step_ms"),
+                  "auto_link_gbs": ctx_stats_final.get("auto_link_gbs"),
                   "note": "gck_recommend_k(n, measured link GB/s, checkpoint-free step time)"},
         "replay": {"host_ms_last_session": st1["last_replay_ms"], "threads": st1["replay_threads"],
                    "worker_ms_last_session": st1["last_worker_ms"],

@@ -179,6 +179,10 @@ typedef struct {
     uint64_t gpu_launches;         /* kernels this context launched */
     int32_t replay_threads;
     int32_t numa_node;             /* node the arena and threads are bound to (-1: unbound) */
+    uint32_t last_session_k;       /* K of the last begun session (K = 0 at begin: chosen automatically) */
+    uint32_t _pad2;
+    double auto_step_ms;           /* step time the last automatic K used (0: not measured) */
+    double auto_link_gbs;          /* link rate the last automatic K used */
 } gck_stats;
 
 /* ---- context lifecycle -------------------------------------------------- */
@@ -199,7 +203,11 @@ gck_status gck_destroy(gck_ctx *ctx);
 /* ---- the session (BJ: begin_checkpoint(step, K), submit, finalize) ------ */
 
 /* Plan a session after step t0 with K parts (a1): parts balanced over
- * A-element units, remainder to the earliest parts. Host-only, no GPU work.
+ * A-element units, remainder to the earliest parts. K = 0 picks K automatically (NEXT-4): the
+ * smallest K in [k_min, k_max] whose largest per-step D2H fits in one step, from the step time
+ * measured between recent submits (cfg.timing) and the link rate of previous drains
+ * (gck_stats.last_session_k reports the choice). Host-only, no GPU work (direct staging also
+ * enqueues part 1's copy).
  * Errors: INVALID (K outside [k_min, k_max] or > ceil(n/A)), PROTOCOL (a
  * session or an unreleased checkpoint is live). */
 gck_status gck_begin_checkpoint(gck_ctx *ctx, uint64_t t0, uint32_t K);

@@ -78,7 +78,9 @@ class Stats(C.Structure):
                 ("d2h_ms_total", C.c_double), ("last_session_stall_ms", C.c_double),
                 ("last_session_d2h_ms", C.c_double), ("last_replay_ms", C.c_double), ("last_worker_ms", C.c_double),
                 ("last_finalize_wait_ms", C.c_double), ("last_session_d2h_bytes", C.c_uint64),
-                ("gpu_launches", C.c_uint64), ("replay_threads", C.c_int32), ("numa_node", C.c_int32)]
+                ("gpu_launches", C.c_uint64), ("replay_threads", C.c_int32), ("numa_node", C.c_int32),
+                ("last_session_k", C.c_uint32), ("_pad2", C.c_uint32), ("auto_step_ms", C.c_double),
+                ("auto_link_gbs", C.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_ if not k.startswith("_")}

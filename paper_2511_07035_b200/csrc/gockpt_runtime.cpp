@@ -19,6 +19,7 @@
 #include <sys/syscall.h>
 #include <unistd.h>
 
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <condition_variable>
@@ -251,6 +252,11 @@ struct gck_ctx {
     cudaStream_t rstream = nullptr;
     char *rscratch = nullptr;
     uint64_t rscratch_bytes = 0;
+
+    // step-time tracking for automatic K (NEXT-4): an event per submit, in a ring
+    static constexpr int kStepEv = 64;
+    cudaEvent_t ev_step[kStepEv]{};
+    uint64_t n_step_ev = 0;
 
     // bias-correction count tracking (the checkpoint records the count of S(T))
     uint64_t count_known = 0;   // count after the last submitted update (0 until known)
@@ -670,6 +676,8 @@ gck_status gck_create(const gck_config *cfg_in, const gck_hparams *hp, const gck
         ok = cudaEventCreateWithFlags(&c->packed[s], cudaEventDisableTiming) == cudaSuccess &&
              cudaEventCreateWithFlags(&c->slot_free[s], cudaEventDisableTiming) == cudaSuccess;
     }
+    for (int i = 0; i < gck_ctx::kStepEv && ok && cfg.timing; ++i)
+        ok = cudaEventCreate(&c->ev_step[i]) == cudaSuccess;
     ok = ok && cudaEventCreateWithFlags(&c->ev_upd, cudaEventDisableTiming) == cudaSuccess &&
          cudaEventCreateWithFlags(&c->ev_grad_src, cudaEventDisableTiming) == cudaSuccess &&
          cudaEventCreateWithFlags(&c->ev_grad_copied, cudaEventDisableTiming) == cudaSuccess;
@@ -710,6 +718,8 @@ gck_status gck_destroy(gck_ctx *c) {
         }
         for (cudaEvent_t ev : {c->ev_upd, c->ev_grad_src, c->ev_grad_copied})
             if (ev) cudaEventDestroy(ev);
+        for (int i = 0; i < gck_ctx::kStepEv; ++i)
+            if (c->ev_step[i]) cudaEventDestroy(c->ev_step[i]);
         if (c->d2h) cudaStreamDestroy(c->d2h);
         if (c->rstream) {
             cudaStreamSynchronize(c->rstream);
@@ -750,12 +760,45 @@ static cudaError_t enqueue_state_copy(gck_ctx *c, uint32_t i) {
     return cudaEventRecord(c->ev_state_copied[i - 1], c->d2h);
 }
 
+// NEXT-4 automatic K: the smallest K in [k_min, k_max] whose largest per-step transfer
+// V_max(K) fits in one measured step at the measured link rate (SURVEY §8(d) K_min;
+// gck_recommend_k). Step time: median of the completed intervals between consecutive submits;
+// link: the bytes / busy time of the previous sessions' drains (50 GB/s before the first).
+static uint32_t auto_k(gck_ctx *c) {
+    std::vector<float> dts;
+    if (c->cfg.timing && c->n_step_ev >= 3) {
+        const uint64_t hi = c->n_step_ev, lo = hi > (uint64_t)gck_ctx::kStepEv ? hi - gck_ctx::kStepEv : 0;
+        for (uint64_t i = lo; i + 1 < hi; ++i) {
+            cudaEvent_t a = c->ev_step[i % gck_ctx::kStepEv], b = c->ev_step[(i + 1) % gck_ctx::kStepEv];
+            if (cudaEventQuery(b) != cudaSuccess) {
+                cudaGetLastError();
+                break;  // later events are not complete either
+            }
+            float ms = 0;
+            if (cudaEventElapsedTime(&ms, a, b) == cudaSuccess && ms > 0) dts.push_back(ms);
+        }
+    }
+    c->stats.auto_step_ms = 0;
+    if (dts.size() < 2) return c->cfg.k_max;
+    std::nth_element(dts.begin(), dts.begin() + dts.size() / 2, dts.end());
+    const double t_step = dts[dts.size() / 2] / 1e3;
+    const double gbs = c->stats.d2h_ms_total > 0 ? (double)c->stats.d2h_bytes / (c->stats.d2h_ms_total * 1e6) : 50.0;
+    c->stats.auto_step_ms = t_step * 1e3;
+    c->stats.auto_link_gbs = gbs;
+    uint32_t k = 0;
+    if (gck_recommend_k(c->cfg.n, c->cfg.part_align, gbs, t_step, 1.0, c->cfg.k_max, &k, nullptr) != GCK_OK || k == 0)
+        return c->cfg.k_max;
+    return std::max(k, c->cfg.k_min);
+}
+
 gck_status gck_begin_checkpoint(gck_ctx *c, uint64_t t0, uint32_t K) {
     if (!c) return set_tls(GCK_E_INVALID, "null ctx");
     if (c->poisoned) return c->fail(GCK_E_CUDA, "context poisoned by an earlier CUDA failure");
     if (c->state != State::IDLE && c->state != State::ABORTED)
         return c->fail(GCK_E_PROTOCOL, "begin_checkpoint while a session or an unreleased checkpoint is live");
+    if (K == 0) K = auto_k(c);  // NEXT-4: pick K from the measured step time and link bandwidth
     if (K < c->cfg.k_min || K > c->cfg.k_max) return c->fail(GCK_E_INVALID, "K outside [k_min, k_max]");
+    c->stats.last_session_k = K;
     if (c->state == State::ABORTED) {  // drain whatever the aborted session left queued
         c->join_worker();
         DeviceGuard g(c->cfg.device);
@@ -972,6 +1015,7 @@ gck_status gck_submit(gck_ctx *c, uint32_t part, const gck_step_args *a, void *s
     f.n = c->cfg.n;
     f.rec = rec;
     c->stats.steps++;
+    if (c->cfg.timing) cudaEventRecord(c->ev_step[c->n_step_ev++ % gck_ctx::kStepEv], s);
 
     if (part == 0) {
         int e = gck::launch_fused(f, false, s, c->num_sms);

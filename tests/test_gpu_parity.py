@@ -563,3 +563,40 @@ def test_two_contexts_interleaved_and_destroy_mid_session(G):
         assert_state_equal((ck.master, ck.exp_avg, ck.exp_avg_sq), want, "interleaved")
         c.release()
         c.close()
+
+
+def test_automatic_k(G):
+    """NEXT-4: begin_checkpoint(t0, 0) picks K from the measured step time and link rate; the
+    session it runs is exact whatever K it picked."""
+    n, t0, seed = 1 << 20, 30, 41
+    state = gi.warm_state(seed, n)
+    p, m, v = (up_f32(x) for x in state)
+    ctx = G.GoCkpt(p, m, v, None, **HP, k_min=1, k_max=16, part_align=1024)
+    ref = tuple(x.copy() for x in state)
+    a = torch.randn(4096, 4096, device="cuda")
+    for s in range(1, t0 + 1):                          # plain steps with some work between them
+        torch.mm(a, a)
+        g = gi.grad_bits(seed, s, n)
+        ctx.submit(0, s, s, 1e-3, up_u16(g))
+        ref = oracle.adamw_update(*ref, g, oracle.make_step_record(t=s, lr=1e-3, **HP))[:3]
+    torch.cuda.synchronize()
+    ctx.begin_checkpoint(t0, 0)
+    st = ctx.stats()
+    K = st["last_session_k"]
+    assert 1 <= K <= 16 and st["auto_step_ms"] > 0
+    target = None
+    for i in range(1, K + 1):
+        s = t0 + i
+        g = gi.grad_bits(seed, s, n)
+        ctx.submit(i, s, s, 1e-3, up_u16(g))
+        ref = oracle.adamw_update(*ref, g, oracle.make_step_record(t=s, lr=1e-3, **HP))[:3]
+        if i == K - 1 or K == 1:
+            target = tuple(x.copy() for x in ref) if K > 1 else target
+    ck = ctx.finalize()
+    if K == 1:
+        target = oracle.trajectory(*state, [gi.grad_bits(seed, s, n) for s in range(1, t0 + 1)],
+                                   [oracle.make_step_record(t=s, lr=1e-3, **HP) for s in range(1, t0 + 1)])[-1]
+    assert ck.step == t0 + K - 1
+    assert_state_equal((ck.master, ck.exp_avg, ck.exp_avg_sq), target, f"auto K={K}")
+    ctx.release()
+    ctx.close()
