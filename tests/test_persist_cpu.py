@@ -114,7 +114,9 @@ def test_crash_during_persist_keeps_previous_latest(G, tmp_path):
     proc = subprocess.Popen([sys.executable, "-c", code2], stdout=subprocess.PIPE, text=True)
     assert proc.stdout.readline().strip() == "go"
     import time
-    time.sleep(0.3)
+    t_end = time.time() + 60
+    while not os.path.exists(tmp_path / "ck_300.bin.tmp") and time.time() < t_end:
+        time.sleep(0.001)                                # kill as soon as the writer has started
     proc.kill()
     proc.wait()
     assert OF.latest(str(tmp_path)) == good
