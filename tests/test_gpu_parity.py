@@ -600,3 +600,37 @@ def test_automatic_k(G):
     assert_state_equal((ck.master, ck.exp_avg, ck.exp_avg_sq), target, f"auto K={K}")
     ctx.release()
     ctx.close()
+
+
+def test_checkpointed_adamw_training_loop(G, tmp_path):
+    """The optimizer face (save_checkpoint / step / wait): checkpoints requested every 12 steps
+    while training runs, each consistent == the oracle's state at its step and durable on disk."""
+    from paper_2511_07035_b200.optim import CheckpointedAdamW
+    from oracle import ckpt_file as OF
+    n, K, seed, steps = 300_007, 4, 51, 40
+    state = gi.warm_state(seed, n)
+    p, m, v = (up_f32(x) for x in state)
+    got = {}
+    opt = CheckpointedAdamW(p, m, v, None, lr=1e-3, K=K, part_align=64, persist_dir=str(tmp_path),
+                            on_checkpoint=lambda ck: got.__setitem__(ck.step, (ck.master.copy(), ck.exp_avg.copy(),
+                                                                               ck.exp_avg_sq.copy())))
+    ref, traj = tuple(x.copy() for x in state), {0: tuple(x.copy() for x in state)}
+    gbuf = torch.empty(n, dtype=torch.int16, device="cuda")
+    for s in range(1, steps + 1):
+        if s % 12 == 1:
+            opt.save_checkpoint()
+        opt.grad_fence()
+        g = gi.grad_bits(seed, s, n)
+        gbuf.copy_(up_u16(g))
+        opt.step(gbuf)
+        ref = oracle.adamw_update(*ref, g, oracle.make_step_record(t=s, lr=1e-3, **HP))[:3]
+        traj[s] = tuple(x.copy() for x in ref)
+    last = opt.wait()
+    opt.close()
+    assert sorted(got) == [K - 1 + 12 * k for k in range(4)] == [3, 15, 27, 39]
+    for step, st in got.items():
+        assert_state_equal(st, traj[step], f"checkpoint at {step}")
+    assert last[0] == 39 and OF.latest(str(tmp_path)) == last[1]
+    hdr, fp, fm, fv = OF.read(last[1])
+    assert hdr["step"] == 39 and hdr["adam_t"] == 39
+    assert_state_equal((fp, fm, fv), traj[39], "persisted")
