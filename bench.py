@@ -60,6 +60,9 @@ def parse():
                     help="partitions per session; 0 = automatic (NEXT-4: chosen by the library from the measured "
                          "step time and link during warm-up, then held for the timed region)")
     ap.add_argument("--model", default="gpt2-small", choices=list(WORKLOADS))
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="nccl (default; the harness's gradient reduce-scatter / param all-gather run on it). "
+                         "gloo = plumbing smoke test with several ranks sharing one GPU: no harness collectives")
     ap.add_argument("--shard-of", type=int, default=0,
                     help="ZeRO-1 data-parallel degree the shard is cut for (0 = the launched world size); "
                          "e.g. 8 on one GPU = one rank of an 8-GPU job")
@@ -199,9 +202,14 @@ def main():
     world, rank, local = dist_env()
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device (there is no CPU fallback)")
+    local = local % torch.cuda.device_count()   # gloo smoke runs may put several ranks on one GPU
     torch.cuda.set_device(local)
+    coll = world > 1 and args.dist_backend == "nccl"   # the harness's NCCL reduce-scatter / all-gather
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     gbuild.build()
     dev = torch.device("cuda", local)
     n, K, I, T = args.n, args.K, args.interval, args.tokens
@@ -220,7 +228,7 @@ def main():
     G.h_generate(G.GEN_EXP_AVG, exp_avg, seed, 0, rank * n)
     G.h_generate(G.GEN_EXP_AVG_SQ, exp_avg_sq, seed, 0, rank * n)
     grad = torch.empty(n, dtype=torch.int16, device=dev)
-    if world > 1:
+    if coll:
         full_grad = torch.empty(n * world, dtype=torch.bfloat16, device=dev)
         full_param = torch.empty(n * world, dtype=torch.bfloat16, device=dev)
     fb = TransformerGemmStandIn(args.model, tokens=T, device=dev)
@@ -267,7 +275,7 @@ def main():
         if h_grad is not None:
             # e2e: the reduced gradient shard arrives from pinned host memory
             grad.copy_(h_grad[s % len(h_grad)], non_blocking=True)
-        elif world > 1:
+        elif coll:
             # backward's full local gradient (harness generator), then the ZeRO-1 reduce-scatter
             G.h_generate(G.GEN_GRAD, full_grad.view(torch.int16), seed, s, 0, 1, 4)
             state["gen"] += 1
@@ -285,7 +293,7 @@ def main():
         if a is not None:
             b.record(stream)
             kern["plain_ms"].append((a, b))
-        if world > 1:
+        if coll:
             dist.all_gather_into_tensor(full_param, param.view(torch.bfloat16))
 
     def baseline_snapshot():
@@ -442,7 +450,7 @@ def main():
                    "fb_standin": f"{args.model} fwd+bwd GEMM chain (cuBLAS bf16, CUDA graph)",
                    "fb_tflop_per_step": fb.flops / 1e12, "copy_mode": args.copy_mode,
                    "ring_slots": args.ring_slots, "staging": args.staging, "scheme": args.scheme,
-                   "replay_mode": args.replay_mode,
+                   "replay_mode": args.replay_mode, "dist_backend": args.dist_backend if world > 1 else None,
                    "parallelism": f"zero1-dp{world}",
                    "l2": f"inputs larger than L2 ({12 * n / 1e9:.2f} GB fp32 state + {2 * n / 1e9:.2f} GB gradient "
                          f"per step per rank)",

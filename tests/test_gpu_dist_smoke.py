@@ -1,0 +1,44 @@
+"""The N>1 bench path end to end on one GPU (-m gpu): torchrun with 2 ranks sharing the device over
+gloo (NCCL refuses two ranks on one GPU; the harness's NCCL collectives are skipped), so per-rank
+ZeRO-1 shards, barrier-bracketed timing with the max over ranks, rank-0-only output and the
+reference arm's rank handling are exercised as the driver's scaling run would."""
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def torchrun(args, timeout=900):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py"), *args]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    return [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+
+
+def test_two_rank_bench_line():
+    lines = torchrun(["--gpus", "2", "--dist-backend", "gloo", "--steps", "2", "--warmup", "3", "--interval", "12",
+                      "--no-e2e"])
+    assert len(lines) == 1
+    d = lines[0]
+    assert d["n_gpus"] == 2 and d["value"] > 0 and d["scaling"] == "weak"
+    assert d["config"]["n_per_rank"] == (124_439_808 + 2 * 512 - 1) // (2 * 512) * 512
+    assert d["gpu_launches"] > 0 and d["roofline"]["achieved"] > 0
+
+
+def test_two_rank_reference_arm():
+    lines = torchrun(["--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "1", "--cpu-sample",
+                      str(1 << 18)])
+    assert len(lines) == 1 and lines[0]["impl"] == "reference" and lines[0]["value"] > 0
