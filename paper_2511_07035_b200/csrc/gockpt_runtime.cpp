@@ -371,7 +371,11 @@ struct gck_ctx {
         {
             DeviceGuard g(cfg.device);
             if (K >= 2) {
-                cudaError_t e = cudaEventSynchronize(done[K - 2]);  // gradient log complete
+                // wait for the LAST drain, not just the gradient log (done[K-2]): the replay's host
+                // DRAM traffic (~135 GB/s on 16 threads) would otherwise compete with the DMA writes
+                // of part K and slow the drain (measured 52 vs 57 GB/s); it costs ~one slot's drain
+                // time of finalize latency
+                cudaError_t e = cudaEventSynchronize(done[K - 1]);
                 if (e != cudaSuccess) st = GCK_E_ABORTED;
             }
             if (st == GCK_OK && !replayed) {
