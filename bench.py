@@ -259,6 +259,7 @@ def main():
     del link, link_h
 
     result_host = []
+    e2e_io = {}
     plain_bytes = 28 * n
     kern = {"plain_ms": [], "plain_bytes": 0, "sess_ms0": 0.0, "sess_n0": 0, "sess_bytes": 0}
 
@@ -270,11 +271,26 @@ def main():
             ev.record(stream)
             step_events.append(ev)
         pre_wait = baseline_snapshot() if snapshot else None   # NEXT-3 baselines: S(t0) = the state now
+        g_in = grad
+        if h_grad is not None:
+            # e2e: the reduced gradient shard arrives from pinned host memory. Like a data loader it is
+            # prefetched on a copy stream into one of two device buffers, overlapping this step's F/B;
+            # the copy starts once the previous update has been enqueued (so the buffer it overwrites,
+            # read by update s-2, is free) and, in direct staging, once the library's copy-out of the
+            # previous gradient slice is done
+            g_in = e2e_io["bufs"][s % 2]
+            begin = torch.cuda.Event()
+            begin.record(stream)
+            loader = e2e_io["stream"]
+            loader.wait_event(begin)
+            ctx.grad_fence(loader)
+            with torch.cuda.stream(loader):
+                g_in.copy_(h_grad[s % len(h_grad)], non_blocking=True)
+            e2e_io["loaded"].record(loader)
         fb()                                                           # F/B stand-in
         ctx.grad_fence(stream)   # direct staging: the last gradient slice is out before we overwrite
         if h_grad is not None:
-            # e2e: the reduced gradient shard arrives from pinned host memory
-            grad.copy_(h_grad[s % len(h_grad)], non_blocking=True)
+            stream.wait_event(e2e_io["loaded"])
         elif coll:
             # backward's full local gradient (harness generator), then the ZeRO-1 reduce-scatter
             G.h_generate(G.GEN_GRAD, full_grad.view(torch.int16), seed, s, 0, 1, 4)
@@ -289,10 +305,12 @@ def main():
         if time_kernel and part == 0:
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             a.record(stream)
-        ctx.submit(part, s, T_WARM + s, LR, grad, 1.0, False, stream)
+        ctx.submit(part, s, T_WARM + s, LR, g_in, 1.0, False, stream)
         if a is not None:
             b.record(stream)
             kern["plain_ms"].append((a, b))
+        if h_grad is not None:   # e2e: the step's result (first 8 bytes of the updated bf16 params) to host
+            result_host[s % 2].copy_(param[:4], non_blocking=True)
         if coll:
             dist.all_gather_into_tensor(full_param, param.view(torch.bfloat16))
 
@@ -402,6 +420,8 @@ def main():
     if not args.no_e2e:
         result_host[:] = [torch.empty(4, dtype=torch.int16, pin_memory=True) for _ in range(2)]
         h_grads = [torch.empty(n, dtype=torch.int16, pin_memory=True) for _ in range(2)]
+        e2e_io.update(bufs=[grad, torch.empty_like(grad)], stream=torch.cuda.Stream(device=dev),
+                      loaded=torch.cuda.Event())
         for k, hg in enumerate(h_grads):
             tmp = torch.empty(n, dtype=torch.int16, device=dev)
             G.h_generate(G.GEN_GRAD, tmp, seed, 10_000 + k, rank * n, 1, 4)
@@ -413,7 +433,8 @@ def main():
         e2e = {"value": max(1, args.steps) * I * T * world / t_e2e, "unit": "tokens/s",
                "h2d_bytes_per_step": 2 * n, "d2h_bytes_per_step": 8 + session_bytes / I,
                "note": "the reduced bf16 gradient shard arrives by H2D from pinned host memory every step "
-                       "(compute stream, inside the timed region; replaces generator + reduce-scatter); each "
+                       "(prefetched on a copy stream into one of two device buffers while the step's F/B runs, "
+                       "inside the timed region; replaces generator + reduce-scatter); each "
                        "step reads 8 bytes of the updated params back (the step's result), and the "
                        "checkpoint the library drains is the session's result (D2H)"}
 
@@ -462,6 +483,9 @@ def main():
                   "ckpt_free_step_ms_median": free_med,
                   "delta_ms_per_session_step_mean": statistics.mean(sess_stall_delta),
                   "delta_ms_per_session_step_max": max(sess_stall_delta),
+                  "delta_ms_per_session_step_median": statistics.median(sess_stall_delta),
+                  "delta_ms_per_session_step_p90": float(np.percentile(sess_stall_delta, 90)),
+                  "session_steps_measured": len(sess_stall_delta),
                   "delta_frac_of_step": statistics.mean(sess_stall_delta) / free_med,
                   "amortized_frac": (t_ck - t_free) / t_free},
         "ckpt_free": {"value": value_free, "unit": "tokens/s", "throughput_ratio": value / value_free,
@@ -477,6 +501,9 @@ def main():
         "replay": {"host_ms_last_session": st1["last_replay_ms"], "threads": st1["replay_threads"],
                    "worker_ms_last_session": st1["last_worker_ms"],
                    "finalize_wait_ms_last": st1["last_finalize_wait_ms"],
+                   "timing_note": "host_ms = the replay arithmetic; worker/finalize_wait are host wall times "
+                                  "from the moment the host enqueued step K (the host runs up to an interval "
+                                  "ahead of the GPU), so they include waiting for the queued steps to execute",
                    "element_updates_per_session": sum((K - 1 - j) * (hi - lo) for j, (lo, hi) in enumerate(parts))},
         "roofline": {"bound": "hbm", "kernel": "fused_adamw_pack (plain step)", "achieved": achieved,
                      "peak": hbm_peak, "unit": "GB/s", "frac": achieved / hbm_peak, "peak_source": peak_src,

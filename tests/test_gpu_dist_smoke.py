@@ -42,3 +42,20 @@ def test_two_rank_reference_arm():
     lines = torchrun(["--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "1", "--cpu-sample",
                       str(1 << 18)])
     assert len(lines) == 1 and lines[0]["impl"] == "reference" and lines[0]["value"] > 0
+
+
+@pytest.mark.parametrize("staging", ["ring", "direct"])
+def test_one_gpu_bench_line_with_e2e(staging):
+    """The default N=1 launch on a reduced shard, e2e leg included: the gradient is prefetched from
+    pinned host memory into alternating device buffers on a copy stream (ring: packed by the fused
+    kernel; direct: copied out of the caller's buffer behind gck_grad_fence)."""
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "2", "--warmup", "3", "--interval", "10",
+           "--K", "4", "--n", str(1 << 24), "--staging", staging, "--no-cpu-baseline"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = lines[0]
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] == 2 * (1 << 24) and e["d2h_bytes_per_step"] > 8
+    assert d["stall"]["session_steps_measured"] == 2 * 4 and d["gpu_launches"] > 0
