@@ -79,6 +79,7 @@ def test_fused_step_trajectory_vs_oracle(G, n):
     (5000, 5, 8, 2, "zerocopy"),
     (64, 8, 8, 1, "ce"),                    # one unit per part
     (1 << 20, 1, 1024, 2, "ce"),            # K=1: a plain snapshot, no gradients
+    (300_007, 64, 8, 2, "ce"),              # K = GCK_K_LIMIT (maximum), TMA kernel, parts not tile-aligned
 ])
 @pytest.mark.parametrize("seed", [42, 7])
 def test_session_staged_replays_and_snapshot(G, n, K, A, R, copy, seed):
