@@ -34,7 +34,7 @@ def row(name, gpus, K, x):
             f"{st['delta_ms_per_session_step_mean']:.2f} ms ({100 * st['delta_frac_of_step']:.2f}% of a "
             f"{st['ckpt_free_step_ms_median']:.1f} ms step) | {x['ckpt_free']['throughput_ratio']:.4f} | "
             f"{x['d2h']['gbs']:.1f} ({100 * x['d2h']['frac']:.1f}%) | {100 * r['frac']:.1f}% plain"
-            + (f", {100 * sess / 6500.6:.1f}% session" if sess else "") + f" @ {x['clocks']['sm_mhz']:.0f} MHz | "
+            + (f", {100 * sess / r['peak']:.1f}% session" if sess else "") + f" @ {x['clocks']['sm_mhz']:.0f} MHz | "
             f"{x['replay']['host_ms_last_session']:.0f} ms |")
 
 
@@ -43,7 +43,8 @@ out = f"""## Results (round 1, measured on one B200 via gpurun; raw lines in `pr
 Stall = event-timed slot/state wait per session step / mean step-time increase of a session
 step over the checkpoint-free median of the same run. Throughput ratio = tokens/s with GoCkpt ÷
 checkpoint-free tokens/s, same run (both ±0.5% run noise). HBM % = fused-kernel algorithmic
-bytes ÷ live CUDA-event time ÷ 6500.6 GB/s (MEASURED_PEAKS). Link % against the best-of-5 1 GiB
+bytes ÷ live CUDA-event time ÷ the pod's measured HBM copy peak (MEASURED_PEAKS: 6500.6 GB/s for the
+C3/C4 rows' pod, 6364.6 GB/s for the C2 row's). Link % against the best-of-5 1 GiB
 D2H of the same run. Parity: every config below is also a `-m gpu` test — checkpoint bit-identical
 to the GPU's own synchronous snapshot over all elements and to the oracle on sampled windows.
 
@@ -82,7 +83,7 @@ to the GPU's own synchronous snapshot over all elements and to the oracle on sam
 - **Persistence** (NEXT-1, `{tag}_persist.txt`): 1.95 GB/s write, ~3 GB/s cold restore on the box's
   virtio disk (GPT-2 shard 0.77 s / 0.54 s; 7B rank shard 5.2 s / 3.2 s).
 - **Sanitizers** (`{tag}_sanitizers.txt`, `{tag}_host_sanitizers.txt`): compute-sanitizer memcheck /
-  racecheck / synccheck clean; ASan+UBSan clean on the host code.
+  racecheck / synccheck clean; ASan+UBSan and TSan clean on the host code.
 - Multi-GPU (2/4/8) was not measured this round: gpurun provides one GPU. `bench.py` runs under
   torchrun (ZeRO-1 shards; NCCL RS/AG in the harness only); the host logic is covered by
   world-size-2 gloo tests.

@@ -635,3 +635,37 @@ def test_checkpointed_adamw_training_loop(G, tmp_path):
     hdr, fp, fm, fv = OF.read(last[1])
     assert hdr["step"] == 39 and hdr["adam_t"] == 39
     assert_state_equal((fp, fm, fv), traj[39], "persisted")
+
+
+# ---------------------------------------------------------------- T2 on one GPU: R shards, R contexts
+@pytest.mark.parametrize("n_total,R,K", [(1_200_007, 4, 4), (300_007, 3, 8)])   # TMA kernel (n_r >= 2^18); grid-stride kernel
+def test_multi_shard_emulation_concatenates_to_global(G, n_total, R, K):
+    """SURVEY §4.2 T2 "single-process multi-shard emulation on one GPU": R contexts over the R ZeRO-1
+    shards of one flat vector (§4.5: every rank saves its own optimizer shard), each driven
+    through the full GPU path (fused kernel + ring + drain + eager host replay) in lock-step from the
+    same global step; the concatenated checkpoints equal the oracle's S(T) of the whole vector."""
+    from paper_2511_07035_b200.harness import zero1_shard
+    t0 = 10
+    _, n_r, padded = zero1_shard(n_total, R, 0, align=1024)
+    ctxs, grads = [], []
+    for r in range(R):
+        idx = np.arange(r * n_r, (r + 1) * n_r, dtype=np.uint64)
+        ctx, _ = _make_ctx(G, gi.warm_state(42, idx), K, part_align=1024, eager_replay=True)
+        ctxs.append(ctx)
+        grads.append([up_u16(gi.grad_bits(42, t0 + i, idx)) for i in range(1, K + 1)])
+    for ctx in ctxs:
+        ctx.begin_checkpoint(t0, K)
+    for i in range(1, K + 1):                      # one global step = every rank's update t0+i
+        for r, ctx in enumerate(ctxs):
+            ctx.submit(i, t0 + i, t0 + i, 1e-3, grads[r][i - 1])
+    cks = [ctx.finalize() for ctx in ctxs]
+    assert all(ck.step == t0 + K - 1 for ck in cks)
+    got = [np.concatenate([getattr(ck, f) for ck in cks]) for f in ("master", "exp_avg", "exp_avg_sq")]
+    idx = np.arange(padded, dtype=np.uint64)
+    p0, m0, v0 = gi.warm_state(42, idx)
+    recs = [oracle.make_step_record(t=t0 + i, lr=1e-3, **HP) for i in range(1, K)]
+    want = oracle.trajectory(p0, m0, v0, [gi.grad_bits(42, t0 + i, idx) for i in range(1, K)], recs)[-1]
+    assert_state_equal(got, want, f"{R} shards concatenated vs oracle S(T)")
+    for ctx in ctxs:
+        ctx.release()
+        ctx.close()
