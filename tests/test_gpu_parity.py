@@ -669,3 +669,33 @@ def test_multi_shard_emulation_concatenates_to_global(G, n_total, R, K):
     for ctx in ctxs:
         ctx.release()
         ctx.close()
+
+
+# ---------------------------------------------------------------- a5 GPU replay kernel, any partition
+@pytest.mark.parametrize("n,K,A,skip_at", [(1000, 2, 1, None), (5003, 5, 3, 2), (100_003, 9, 1, None),
+                                           (300_007, 17, 8, 5), (2_000_003, 8, 1024, None), (65, 64, 1, 7)])
+def test_replay_device_any_partition_vs_oracle(G, n, K, A, skip_at):
+    """gck_replay_device (the part-interleaved replay kernel) on partitions whose boundaries are not
+    8-element aligned (A = 1, 3), up to K = 64 parts, with a skipped update: the replayed state equals
+    the oracle's O2 replay (and so S(T), O1) bit for bit."""
+    t0, seed = 10, 3
+    p0, m0, v0 = gi.warm_state(seed, n)
+    grads = [gi.grad_bits(seed, t0 + i, n) for i in range(1, K + 1)]
+    orecs, lrecs, t = [], [], t0
+    for i in range(1, K + 1):
+        sk = (i == skip_at)
+        t += 0 if sk else 1
+        orecs.append(oracle.make_step_record(t=max(t, 1), lr=1e-3, skip=sk, **HP))
+        lrecs.append(G.make_step_record(HP["beta1"], HP["beta2"], HP["eps"], HP["weight_decay"], max(t, 1), 1e-3,
+                                        skip=sk))
+    parts = oracle.make_parts(n, K, A)
+    assert G.plan_parts(n, K, A) == parts
+    cap, glog, _ = oracle.capture_session(p0, m0, v0, grads, orecs, parts)
+    want = oracle.replay(cap, glog, orecs, parts)
+    dp, dm, dv = (up_f32(np.ascontiguousarray(x)) for x in oracle.assemble(cap))
+    dg = [up_u16(np.ascontiguousarray(g)) for g in glog]
+    G.replay_device(lrecs, parts, dp, dm, dv, dg)
+    torch.cuda.synchronize()
+    assert_state_equal((down_f32(dp), down_f32(dm), down_f32(dv)), want, "GPU replay vs oracle O2")
+    traj = oracle.trajectory(p0, m0, v0, grads[:K - 1], orecs[:K - 1])
+    assert_state_equal((down_f32(dp), down_f32(dm), down_f32(dv)), traj[-1], "GPU replay vs oracle O1")
