@@ -68,8 +68,9 @@ to the GPU's own synchronous snapshot over all elements and to the oracle on sam
 - **Replay:** host pool {hr['runs'][-1]['ms']:.1f} ms for {hr['element_updates'] / 1e6:.0f}M element-updates at
   {hr['runs'][-1]['threads']} threads = {hr['runs'][-1]['gbs']:.0f} GB/s = {100 * hr['runs'][-1]['frac_of_triad']:.0f}% of the box's STREAM
   triad ({hr['runs'][-1]['triad_gbs']:.0f} GB/s); 1 thread {hr['runs'][0]['ms']:.0f} ms. GPU replay kernel {mr['us_mean']:.0f} µs =
-  {mr['gbs']:.0f} GB/s ({100 * mr['frac_of_6500']:.0f}% of HBM; ~45 instructions per element-update make it
-  issue-bound at ~70% of the SM issue rate as well).
+  {mr['gbs']:.0f} GB/s ({100 * mr['frac_of_6500']:.0f}% of HBM) — but the bound is issue, not HBM: 45.6 warp-instructions
+  per 32 element-updates, ncu issue-active 80%, 79% of the issue roofline (553 µs at 1.9 GHz); a part-interleaved
+  variant was slower (`{tag}_replay_interleave_experiment.txt`).
 - **CPU oracle on one host core** (`--impl reference`, 2^20-element sample scaled): {ref['value']:.0f}
   tokens/s-equivalent; {d['cpu_baseline']['value']:.0f} with the 2^24 sample of the bench's cpu_baseline leg
   (AdamW + capture + replay only, no F/B).
