@@ -487,6 +487,11 @@ def main():
                   "delta_ms_per_session_step_p90": float(np.percentile(sess_stall_delta, 90)),
                   "session_steps_measured": len(sess_stall_delta),
                   "delta_frac_of_step": statistics.mean(sess_stall_delta) / free_med,
+                  "delta_ms_vs_plain_steps_same_intervals": statistics.mean(sess_ms) - statistics.median(plain_ms_steps),
+                  "delta_note": "delta_* compare session steps with the checkpoint-free run measured before and after "
+                                "the timed region (clock/thermal drift between the regions shows up in it: compare "
+                                "plain_step_ms_median with ckpt_free_step_ms_median); *_vs_plain_steps_same_intervals "
+                                "compares them with the plain steps of the same timed intervals",
                   "amortized_frac": (t_ck - t_free) / t_free},
         "ckpt_free": {"value": value_free, "unit": "tokens/s", "throughput_ratio": value / value_free,
                       "how": "checkpoint-free intervals measured before and after the timed region, same run"},
