@@ -36,7 +36,10 @@ for d in s:
     name = c["scheme"] + ("" if c["scheme"] != "gockpt" else
                           {"direct": "-O (direct)", "ring": " (ring)", "blocking": " (paper, blocking)"}[c["staging"]])
     per = st["delta_ms_per_session_step_mean"] * (1 if c["scheme"] != "gockpt" else c["K"])
+    same = st.get("delta_ms_vs_plain_steps_same_intervals")
+    same_s = (f"   (vs plain steps of the same intervals: "
+              f"{same * (1 if c['scheme'] != 'gockpt' else c['K']):8.2f} ms/ckpt)" if same is not None else "")
     lines.append(f"{c['workload'][:32]:32s} {name:26s} {per:9.2f} ms/ckpt   throughput ratio "
-                 f"{d['ckpt_free']['throughput_ratio']:.4f}   step {st['ckpt_free_step_ms_median']:.1f} ms")
+                 f"{d['ckpt_free']['throughput_ratio']:.4f}   step {st['ckpt_free_step_ms_median']:.1f} ms" + same_s)
 open(P + f"{tag}_k_sweep_and_schemes.txt", "w").write("\n".join(lines) + "\n")
 print("\n".join(lines))

@@ -4,6 +4,10 @@ import sys
 
 tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
 P = "profiles/"
+try:
+    HBM = json.load(open("MEASURED_PEAKS.json"))["hbm_gbs"]
+except (OSError, KeyError, ValueError):
+    HBM = 6500.6
 
 
 def last_json(path):
@@ -38,13 +42,33 @@ def row(name, gpus, K, x):
             f"{x['replay']['host_ms_last_session']:.0f} ms |")
 
 
+SCH = [json.loads(l) for l in open(P + f"{tag}_schemes.jsonl") if l.startswith("{")]
+
+
+def _per_ckpt(d):
+    st, c = d["stall"], d["config"]
+    return st["delta_ms_per_session_step_mean"] * (1 if c["scheme"] != "gockpt" else c["K"])
+
+
+def _name(c):
+    return {"sync": "Sync", "async-o": "Async-O"}.get(c["scheme"]) or {
+        "ring": "ring GoCkpt", "direct": "GoCkpt-O", "blocking": "paper-faithful GoCkpt (blocking gradient D2H)"}[c["staging"]]
+
+
+def schemes(prefix):
+    return ", ".join(f"{_name(d['config'])} {_per_ckpt(d):.1f} ms" for d in SCH if d["config"]["workload"].startswith(prefix))
+
+
+_l13 = {_name(d["config"]): _per_ckpt(d) for d in SCH if d["config"]["workload"].startswith("Llama-2 13B")}
+ratio_o = _l13["GoCkpt-O"] / _l13["Async-O"]
+
 out = f"""## Results (round 1, measured on one B200 via gpurun; raw lines in `profiles/{tag}_*`)
 
 Stall = event-timed slot/state wait per session step / mean step-time increase of a session
 step over the checkpoint-free median of the same run. Throughput ratio = tokens/s with GoCkpt ÷
 checkpoint-free tokens/s, same run (both ±0.5% run noise). HBM % = fused-kernel algorithmic
-bytes ÷ live CUDA-event time ÷ the pod's measured HBM copy peak (MEASURED_PEAKS: 6500.6 GB/s for the
-C3/C4 rows' pod, 6364.6 GB/s for the C2 row's). Link % against the best-of-5 1 GiB
+bytes ÷ live CUDA-event time ÷ the measured HBM copy peak in MEASURED_PEAKS.json ({HBM} GB/s this round;
+bench.py reads it at run time). Link % against the best-of-5 1 GiB
 D2H of the same run. Parity: every config below is also a `-m gpu` test — checkpoint bit-identical
 to the GPU's own synchronous snapshot over all elements and to the oracle on sampled windows.
 
@@ -62,23 +86,22 @@ to the GPU's own synchronous snapshot over all elements and to the oracle on sam
   {d['clocks']['sm_mhz']:.0f} MHz (power-capped); e2e (gradient H2D from pinned host + result read each step)
   {d['e2e']['value']:.0f} tokens/s; {d['gpu_launches']} of our kernels in the timed region.
 {long_line}- **Fused AdamW+pack kernel:** {mf['plain_us_mean']:.0f} µs = {mf['plain_gbs']:.0f} GB/s =
-  {100 * mf['plain_gbs'] / 6500.6:.1f}% of the measured HBM copy in isolation (session launches
+  {100 * mf['plain_gbs'] / HBM:.1f}% of the measured HBM copy in isolation (session launches
   {mf['session_gbs']:.0f} GB/s); live in the bench {100 * d['roofline']['frac']:.1f}%; ncu: DRAM bytes = the algorithmic 28n;
   a plain 8-stream copy of the same pattern tops out at 5.6–6.16 TB/s (`{tag}_stream8.txt`).
 - **Replay:** host pool {hr['runs'][-1]['ms']:.1f} ms for {hr['element_updates'] / 1e6:.0f}M element-updates at
   {hr['runs'][-1]['threads']} threads = {hr['runs'][-1]['gbs']:.0f} GB/s = {100 * hr['runs'][-1]['frac_of_triad']:.0f}% of the box's STREAM
   triad ({hr['runs'][-1]['triad_gbs']:.0f} GB/s); 1 thread {hr['runs'][0]['ms']:.0f} ms. GPU replay kernel {mr['us_mean']:.0f} µs =
-  {mr['gbs']:.0f} GB/s ({100 * mr['frac_of_6500']:.0f}% of HBM) — but the bound is issue, not HBM: 45.6 warp-instructions
+  {mr['gbs']:.0f} GB/s ({100 * mr['gbs'] / HBM:.0f}% of HBM) — but the bound is issue, not HBM: 45.6 warp-instructions
   per 32 element-updates, ncu issue-active 80%, 79% of the issue roofline (553 µs at 1.9 GHz); a part-interleaved
   variant was slower (`{tag}_replay_interleave_experiment.txt`).
 - **CPU oracle on one host core** (`--impl reference`, 2^20-element sample scaled): {ref['value']:.0f}
   tokens/s-equivalent; {d['cpu_baseline']['value']:.0f} with the 2^24 sample of the bench's cpu_baseline leg
   (AdamW + capture + replay only, no F/B).
 - **Stall vs the paper's schemes on B200** (NEXT-3, `{tag}_k_sweep_and_schemes.txt`, one run), per
-  checkpoint: GPT-2 — Sync 25.6 ms, Async-O 9.5 ms, paper-faithful GoCkpt (blocking gradient D2H)
-  14.5 ms, this build's ring GoCkpt 1.9 ms, GoCkpt-O 1.6 ms; Llama-2 13B rank-of-8 shard —
-  332 / 197 / 174 / 14.9 / 9.8 ms (GoCkpt-O = 5% of Async-O's stall; the paper reports 0.5–10% on
-  V100S, P:452).
+  checkpoint (session-step delta × K vs the checkpoint-free run): GPT-2 — {schemes('GPT-2')};
+  Llama-2 13B rank-of-8 shard — {schemes('Llama-2 13B')}. GoCkpt-O's stall is {100 * ratio_o:.0f}% of
+  Async-O's on the 13B shard (the paper reports 0.5–10% on V100S, P:452).
 - **C5 D2H sweep** (`{tag}_d2h_sweep.txt`): copy engine 56–57 GB/s from 16 MiB to 8 GiB;
   zero-copy 50–52.7 GB/s, 20–44 GB/s under a concurrent GEMM; 4 MiB chunks (P:362) cost ~5%.
 - **Persistence** (NEXT-1, `{tag}_persist.txt`): 1.95 GB/s write, ~3 GB/s cold restore on the box's
