@@ -74,7 +74,7 @@ typedef struct {
 } gck_hparams;
 
 enum { GCK_COPY_ENGINE = 0, GCK_COPY_ZEROCOPY = 1 };
-enum { GCK_REPLAY_HOST = 0, GCK_REPLAY_GPU = 1 };
+enum { GCK_REPLAY_HOST = 0, GCK_REPLAY_GPU = 1, GCK_REPLAY_DEFERRED = 2 };
 enum { GCK_STAGE_RING = 0, GCK_STAGE_DIRECT = 1, GCK_STAGE_BLOCKING = 2 };
 
 typedef struct {
@@ -93,7 +93,12 @@ typedef struct {
     int32_t replay_mode;    /* GCK_REPLAY_HOST: the host thread pool replays in place;
                                GCK_REPLAY_GPU: the stale parts + gradient log go back up to HBM, the
                                replay kernel runs there, the consistent parts come back (no host
-                               arithmetic; library-owned device scratch allocated on first use) */
+                               arithmetic; library-owned device scratch allocated on first use);
+                               GCK_REPLAY_DEFERRED (replay-on-restore): finalize
+                               does no replay — the handle holds the captured parts (replay_pending = 1),
+                               gck_persist_begin writes them with the gradient log and StepRecords
+                               (file version 2), and the replay runs at load time: on the GPU inside
+                               gck_restore, on the host inside gck_load_checkpoint(_range) */
     int32_t replay_threads; /* host replay threads (0 -> all cores of the affinity mask) */
     int32_t timing;         /* 1: record CUDA events for stall / kernel / D2H times (gck_stats) */
     int32_t eager_replay;   /* 1: replay starts on a library thread as soon as the gradient log is
@@ -151,6 +156,9 @@ typedef struct {
     uint64_t step;              /* = T = t0 + K - 1 */
     uint64_t n;
     const float *master, *exp_avg, *exp_avg_sq;
+    uint32_t K;                 /* the session's K */
+    uint32_t replay_pending;    /* 1 (GCK_REPLAY_DEFERRED only): master/m/v still hold part i at
+                                   S(t0+i-1); S(T) is materialised when the persisted file is loaded */
 } gck_checkpoint;
 
 /* The staged (pre-replay) host bytes of the current session, for verification:
@@ -339,11 +347,12 @@ typedef struct {
 gck_status gck_write_checkpoint(const char *path, const gck_file_header *hdr, const float *master, const float *m,
                                 const float *v, int32_t threads, const char *meta_json, gck_persist_stats *stats);
 
-/* Read and validate (magic, version, header CRC) a checkpoint file's header. Host-only. */
+/* Read and validate (magic, version 1 or 2, header CRC) a checkpoint file's header. Host-only. */
 gck_status gck_read_header(const char *path, gck_file_header *out);
 
 /* Read a checkpoint file into host arrays of n floats each, verifying every block CRC
- * ("first read from the SSD into CPU memory"). Host-only, blocking.
+ * ("first read from the SSD into CPU memory"). A version-2 file is replayed on the host
+ * (`threads` threads) after the read, so the arrays receive S(T) either way. Host-only, blocking.
  * Errors: INVALID (n mismatch), IO, CORRUPT. */
 gck_status gck_load_checkpoint(const char *path, uint64_t n, float *master, float *m, float *v, int32_t threads,
                                gck_file_header *out, gck_persist_stats *stats);
@@ -351,13 +360,56 @@ gck_status gck_load_checkpoint(const char *path, uint64_t n, float *master, floa
 /* Read elements [offset, offset + count) of a checkpoint file's master / m / v into host arrays of
  * count floats; every 64 MiB block the range touches is read whole and CRC-verified. For loading
  * into a different ZeRO-1 degree: a new rank's range spans parts of old ranks' files.
- * Host-only. Errors: INVALID (range outside n), IO, CORRUPT. */
+ * A version-2 file also reads the gradient slices over the range and replays it (S(T)). Host-only. Errors: INVALID (range outside n), IO, CORRUPT. */
 gck_status gck_load_checkpoint_range(const char *path, uint64_t offset, uint64_t count, float *master, float *m,
                                      float *v, int32_t threads, gck_file_header *out);
 
+/* ---- NEXT-2: replay-on-restore (file version 2) ------------------------------------------
+ * A version-2 file is a version-1 file whose three sections hold the session's CAPTURED parts
+ * (part i = [lo_i, hi_i) at S(t0+i-1), §4.2.1) instead of S(T), followed by the replay
+ * log: at offset L (= the end of a version-1 file of the same n, i.e. section_offset[2] +
+ * section_bytes[2] rounded up to 4096) one gck_log_header (padded to 8192 bytes), at
+ * glog_table_offset the per-block CRC-32 table of the gradient slices (glog_nblocks entries,
+ * slices in order, each slice split into block_bytes blocks), and each slice i < K
+ * (G(t0+i)[0:hi_i], bf16 bits, "G_A^1 and G_AB^2") at glog_offset[i-1], 4096-aligned.
+ * Loading applies updates t0+j .. T to every part j < K in ascending order with rec[] — the
+ * same per-element op sequence as the session replay (§4.3.1) — so the loaded state
+ * is S(T) bit for bit. header.step = T and header.adam_t = t(T), as in version 1. */
+#define GCK_FILE_VERSION_LOG 2u
+#define GCK_LOG_MAGIC "GCKRLOG\0"
+#define GCK_LOG_HEADER_BYTES 8192u
+
+typedef struct {
+    char magic[8];                          /* GCK_LOG_MAGIC */
+    uint32_t K, _pad;                       /* session K, 1..GCK_K_LIMIT */
+    uint64_t t0;                            /* the session began after update t0; T = t0 + K - 1 */
+    uint64_t lo[GCK_K_LIMIT], hi[GCK_K_LIMIT];  /* part i = [lo[i-1], hi[i-1]); zero beyond K */
+    gck_step_record rec[GCK_K_LIMIT];       /* rec[i-1] = StepRecord of update t0+i, i = 1..K */
+    uint64_t glog_offset[GCK_K_LIMIT];      /* file offset of slice i (i < K; hi[i-1] bf16); else 0 */
+    uint64_t glog_table_offset, glog_nblocks;
+    uint32_t glog_table_crc;                /* CRC-32 of the glog_nblocks table entries */
+    uint32_t log_crc;                       /* CRC-32 of every byte of this struct before this field */
+} gck_log_header;
+
+/* Write a version-2 (replay-on-restore) file: master/m/v are the captured host arrays (n floats
+ * each; part i at S(t0+i-1)), lo_hi the K parts as 2K uint64 (the a1 plan: contiguous,
+ * ascending, covering [0, n)), recs the K StepRecords of updates t0+1 .. t0+K, glog[i] (i < K-1)
+ * the host gradient slice of update t0+i+1 with hi_{i+1} elements. Same atomic publication as
+ * gck_write_checkpoint. Host-only, blocking. Errors: INVALID (K, plan or pointers), IO, ABORTED. */
+gck_status gck_write_checkpoint_log(const char *path, const gck_file_header *hdr, const float *master,
+                                    const float *m, const float *v, uint32_t K, uint64_t t0,
+                                    const uint64_t *lo_hi, const gck_step_record *recs,
+                                    const uint16_t *const *glog, int32_t threads, const char *meta_json,
+                                    gck_persist_stats *stats);
+
+/* Read and validate (magic, log CRC, plan) the replay log header of a version-2 file.
+ * Errors: INVALID (a version-1 file), IO, CORRUPT. Host-only. */
+gck_status gck_read_log_header(const char *path, gck_log_header *out);
+
 /* Persist the finalized checkpoint (state READY) in the background on a library thread;
  * gck_release (and gck_destroy) wait for it, so the next session cannot begin before the
- * previous checkpoint is durable ("GoCkpt will wait for the last checkpoint"). */
+ * previous checkpoint is durable ("GoCkpt will wait for the last checkpoint").
+ * With GCK_REPLAY_DEFERRED the file is version 2 (captured parts + gradient log + records). */
 gck_status gck_persist_begin(gck_ctx *ctx, const char *path, uint32_t rank, uint32_t world, const char *meta_json);
 
 /* Wait for the background persist; returns its status and stats. */
@@ -365,7 +417,11 @@ gck_status gck_persist_wait(gck_ctx *ctx, gck_persist_stats *out);
 
 /* Restore (no session live): load `path` into the pinned arena, upload master/m/v into the
  * context's device tensors on `stream`, re-derive the bf16 working copy RNE(master), and
- * synchronize ("then transferred to GPU memory ... resumed at the step after"). */
+ * synchronize ("then transferred to GPU memory ... resumed at the step after").
+ * A version-2 file's gradient slices go up to temporary device memory and the replay kernel
+ * brings the stale parts to S(T) in place on the device tensors before the bf16 cast
+ * (replay-on-restore: HBM-speed reconstruction, no host arithmetic). A version-2 file's K may
+ * exceed the context's k_max. Errors: PROTOCOL, INVALID (n mismatch), IO, CORRUPT, NOMEM, CUDA. */
 gck_status gck_restore(gck_ctx *ctx, const char *path, void *stream, gck_file_header *out);
 
 /* ---- NEXT-4: analytic model (§3.1; §4.2.3) and K selection ------ */

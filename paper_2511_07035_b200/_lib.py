@@ -25,7 +25,7 @@ K_LIMIT = 64
 STATUS_NAMES = ["GCK_OK", "GCK_E_INVALID", "GCK_E_PROTOCOL", "GCK_E_STALE", "GCK_E_NOMEM", "GCK_E_CUDA",
                 "GCK_E_INCOMPLETE", "GCK_E_ABORTED", "GCK_E_BUSY", "GCK_E_NODEVICE", "GCK_E_IO", "GCK_E_CORRUPT"]
 COPY_ENGINE, COPY_ZEROCOPY = 0, 1
-REPLAY_HOST, REPLAY_GPU = 0, 1
+REPLAY_HOST, REPLAY_GPU, REPLAY_DEFERRED = 0, 1, 2
 STAGE_RING, STAGE_DIRECT, STAGE_BLOCKING = 0, 1, 2
 
 
@@ -61,7 +61,7 @@ class StepRecord(C.Structure):
 
 class Checkpoint(C.Structure):
     _fields_ = [("step", C.c_uint64), ("n", C.c_uint64), ("master", C.c_void_p), ("exp_avg", C.c_void_p),
-                ("exp_avg_sq", C.c_void_p)]
+                ("exp_avg_sq", C.c_void_p), ("K", C.c_uint32), ("replay_pending", C.c_uint32)]
 
 
 class Staged(C.Structure):
@@ -93,6 +93,13 @@ class FileHeader(C.Structure):
                 ("weight_decay", C.c_double), ("block_bytes", C.c_uint64), ("nblocks", C.c_uint64),
                 ("table_offset", C.c_uint64), ("section_offset", C.c_uint64 * 3), ("section_bytes", C.c_uint64 * 3),
                 ("table_crc", C.c_uint32), ("header_crc", C.c_uint32)]
+
+
+class LogHeader(C.Structure):
+    _fields_ = [("magic", C.c_char * 8), ("K", C.c_uint32), ("_pad", C.c_uint32), ("t0", C.c_uint64),
+                ("lo", C.c_uint64 * K_LIMIT), ("hi", C.c_uint64 * K_LIMIT), ("rec", StepRecord * K_LIMIT),
+                ("glog_offset", C.c_uint64 * K_LIMIT), ("glog_table_offset", C.c_uint64),
+                ("glog_nblocks", C.c_uint64), ("glog_table_crc", C.c_uint32), ("log_crc", C.c_uint32)]
 
 
 class PersistStats(C.Structure):
@@ -136,6 +143,10 @@ SIGNATURES = {
     "gck_write_checkpoint": (C.c_int, [C.c_char_p, C.POINTER(FileHeader), P, P, P, C.c_int32, C.c_char_p,
                                        C.POINTER(PersistStats)]),
     "gck_read_header": (C.c_int, [C.c_char_p, C.POINTER(FileHeader)]),
+    "gck_write_checkpoint_log": (C.c_int, [C.c_char_p, C.POINTER(FileHeader), P, P, P, C.c_uint32, C.c_uint64,
+                                           U64P, C.POINTER(StepRecord), C.POINTER(P), C.c_int32, C.c_char_p,
+                                           C.POINTER(PersistStats)]),
+    "gck_read_log_header": (C.c_int, [C.c_char_p, C.POINTER(LogHeader)]),
     "gck_load_checkpoint": (C.c_int, [C.c_char_p, C.c_uint64, P, P, P, C.c_int32, C.POINTER(FileHeader),
                                       C.POINTER(PersistStats)]),
     "gck_load_checkpoint_range": (C.c_int, [C.c_char_p, C.c_uint64, C.c_uint64, P, P, P, C.c_int32,

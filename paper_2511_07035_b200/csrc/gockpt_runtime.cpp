@@ -378,7 +378,8 @@ struct gck_ctx {
                 cudaError_t e = cudaEventSynchronize(done[K - 1]);
                 if (e != cudaSuccess) st = GCK_E_ABORTED;
             }
-            if (st == GCK_OK && !replayed) {
+            // replay-on-restore: the stale parts stay as captured; the load replays them
+            if (st == GCK_OK && !replayed && cfg.replay_mode != GCK_REPLAY_DEFERRED) {
                 const uint16_t *gl[GCK_K_LIMIT];
                 for (uint32_t i = 0; i < K; ++i) gl[i] = glog[i];
                 const auto r0 = std::chrono::steady_clock::now();
@@ -596,7 +597,8 @@ gck_status gck_create(const gck_config *cfg_in, const gck_hparams *hp, const gck
         return set_tls(GCK_E_INVALID, "bad staging");
     if (cfg.copy_mode != GCK_COPY_ENGINE && cfg.copy_mode != GCK_COPY_ZEROCOPY)
         return set_tls(GCK_E_INVALID, "bad copy_mode");
-    if (cfg.replay_mode != GCK_REPLAY_HOST && cfg.replay_mode != GCK_REPLAY_GPU)
+    if (cfg.replay_mode != GCK_REPLAY_HOST && cfg.replay_mode != GCK_REPLAY_GPU &&
+        cfg.replay_mode != GCK_REPLAY_DEFERRED)
         return set_tls(GCK_E_INVALID, "bad replay_mode");
     if (!(hp->beta1 > 0 && hp->beta1 < 1 && hp->beta2 > 0 && hp->beta2 < 1 && hp->eps > 0 && hp->weight_decay >= 0))
         return set_tls(GCK_E_INVALID, "hyperparameters out of range");
@@ -1159,6 +1161,8 @@ static gck_status finalize_impl(gck_ctx *c, gck_checkpoint *out, bool block) {
     out->master = c->h_master;
     out->exp_avg = c->h_m;
     out->exp_avg_sq = c->h_v;
+    out->K = c->K;
+    out->replay_pending = (c->cfg.replay_mode == GCK_REPLAY_DEFERRED && c->K > 1) ? 1u : 0u;
     return GCK_OK;
 }
 
@@ -1255,6 +1259,43 @@ gck_status gck_write_checkpoint(const char *path, const gck_file_header *hdr, co
     return st == GCK_OK ? st : set_tls(st, err);
 }
 
+gck_status gck_write_checkpoint_log(const char *path, const gck_file_header *hdr, const float *master,
+                                    const float *m, const float *v, uint32_t K, uint64_t t0,
+                                    const uint64_t *lo_hi, const gck_step_record *recs,
+                                    const uint16_t *const *glog, int32_t threads, const char *meta_json,
+                                    gck_persist_stats *stats) {
+    if (!path || !hdr || !master || !m || !v || !lo_hi || !recs || (K > 1 && !glog))
+        return set_tls(GCK_E_INVALID, "null argument");
+    if (hdr->n == 0) return set_tls(GCK_E_INVALID, "n must be >= 1");
+    if (K < 1 || K > GCK_K_LIMIT) return set_tls(GCK_E_INVALID, "K outside 1..64");
+    if (hdr->step != t0 + K - 1) return set_tls(GCK_E_INVALID, "hdr->step must be t0 + K - 1");
+    gck::ReplayLog log;
+    log.K = K;
+    log.t0 = t0;
+    for (uint32_t i = 0; i < K; ++i) {
+        log.lo[i] = lo_hi[2 * i];
+        log.hi[i] = lo_hi[2 * i + 1];
+        log.rec[i] = recs[i];
+        if (i + 1 < K) {
+            if (!glog[i]) return set_tls(GCK_E_INVALID, "null gradient slice");
+            log.glog[i] = glog[i];
+        }
+    }
+    const std::string pe = gck::plan_error(K, log.lo, log.hi, hdr->n);
+    if (!pe.empty()) return set_tls(GCK_E_INVALID, "plan: " + pe);
+    const float *sec[3] = {master, m, v};
+    std::string err;
+    const gck_status st = gck::write_checkpoint_impl(path, hdr, sec, threads, meta_json, stats, &err, &log);
+    return st == GCK_OK ? st : set_tls(st, err);
+}
+
+gck_status gck_read_log_header(const char *path, gck_log_header *out) {
+    if (!path || !out) return set_tls(GCK_E_INVALID, "null argument");
+    std::string err;
+    const gck_status st = gck::read_log_header_impl(path, out, &err);
+    return st == GCK_OK ? st : set_tls(st, err);
+}
+
 gck_status gck_read_header(const char *path, gck_file_header *out) {
     if (!path || !out) return set_tls(GCK_E_INVALID, "null argument");
     std::string err;
@@ -1299,13 +1340,26 @@ gck_status gck_persist_begin(gck_ctx *c, const char *path, uint32_t rank, uint32
     c->persist_status = GCK_OK;
     c->persist_error.clear();
     c->persist_started = true;
-    c->persist_worker = std::thread([c, h, p, meta]() {
+    // replay-on-restore: the captured parts go out with the gradient log and the StepRecords
+    const bool deferred = c->cfg.replay_mode == GCK_REPLAY_DEFERRED && c->K > 1;
+    c->persist_worker = std::thread([c, h, p, meta, deferred]() {
         if (c->numa >= 0) pthread_setaffinity_np(pthread_self(), sizeof(cpu_set_t), &c->numa_cpus);
         const float *sec[3] = {c->h_master, c->h_m, c->h_v};
+        gck::ReplayLog log;
+        if (deferred) {
+            log.K = c->K;
+            log.t0 = c->t0;
+            for (uint32_t i = 0; i < c->K; ++i) {
+                log.lo[i] = c->lo[i];
+                log.hi[i] = c->hi[i];
+                log.rec[i] = c->recs[i];
+                log.glog[i] = (i + 1 < c->K) ? c->glog[i] : nullptr;
+            }
+        }
         std::string err;
         gck_persist_stats ps{};
         const gck_status st = gck::write_checkpoint_impl(p.c_str(), &h, sec, c->cfg.replay_threads, meta.c_str(),
-                                                         &ps, &err);
+                                                         &ps, &err, deferred ? &log : nullptr);
         c->persist_stats = ps;
         c->persist_status = st;
         c->persist_error = err;
@@ -1329,7 +1383,10 @@ gck_status gck_restore(gck_ctx *c, const char *path, void *stream, gck_file_head
     float *dst[3] = {c->h_master, c->h_m, c->h_v};
     std::string err;
     gck_file_header h;
-    gck_status st = gck::load_checkpoint_impl(path, dst, c->cfg.n, c->cfg.replay_threads, &h, nullptr, &err);
+    gck::LoadedLog log;  // version 2: slices into the pinned arena's gradient log when they fit
+    log.buf = c->h_glog;
+    log.buf_elems = c->glog_elems_cap;
+    gck_status st = gck::load_checkpoint_impl(path, dst, c->cfg.n, c->cfg.replay_threads, &h, nullptr, &err, &log);
     if (st != GCK_OK) return c->fail(st, err);
     DeviceGuard g(c->cfg.device);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -1339,6 +1396,39 @@ gck_status gck_restore(gck_ctx *c, const char *path, void *stream, gck_file_head
         (e = cudaMemcpyAsync(c->t.exp_avg, c->h_m, b, cudaMemcpyHostToDevice, s)) != cudaSuccess ||
         (e = cudaMemcpyAsync(c->t.exp_avg_sq, c->h_v, b, cudaMemcpyHostToDevice, s)) != cudaSuccess)
         return c->cuda_fail(e, "restore upload");
+    if (log.present && log.lh.K > 1) {
+        // replay-on-restore (NEXT-2): slices -> temporary HBM, replay kernel in place on the
+        // device tensors (parts j < K from S(t0+j) to S(T)), same op sequence as every replay
+        const gck_log_header &lh = log.lh;
+        uint64_t need = 0, goff[GCK_K_LIMIT] = {};
+        for (uint32_t i = 0; i + 1 < lh.K; ++i) {
+            goff[i] = need;
+            need += align_up(lh.hi[i] * 2, 256);
+        }
+        char *dg = nullptr;
+        if ((e = cudaMallocAsync((void **)&dg, need, s)) != cudaSuccess) return c->cuda_fail(e, "restore scratch");
+        gck::ReplayArgs ra;
+        std::memset(&ra, 0, sizeof(ra));
+        ra.p = c->t.master;
+        ra.m = c->t.exp_avg;
+        ra.v = c->t.exp_avg_sq;
+        ra.K = lh.K;
+        ra.n_replay = lh.hi[lh.K - 2];
+        for (uint32_t i = 0; i < lh.K; ++i) {
+            ra.lo[i] = lh.lo[i];
+            ra.hi[i] = lh.hi[i];
+            ra.rec[i] = lh.rec[i];
+            if (i + 1 < lh.K) {
+                ra.glog[i] = reinterpret_cast<const uint16_t *>(dg + goff[i]);
+                if ((e = cudaMemcpyAsync(dg + goff[i], log.glog[i], lh.hi[i] * 2, cudaMemcpyHostToDevice, s)) !=
+                    cudaSuccess)
+                    return c->cuda_fail(e, "restore gradient upload");
+            }
+        }
+        if (gck::launch_replay(ra, stream, c->num_sms)) return c->cuda_fail(cudaGetLastError(), "restore replay");
+        c->stats.gpu_launches++;
+        if ((e = cudaFreeAsync(dg, s)) != cudaSuccess) return c->cuda_fail(e, "restore scratch free");
+    }
     if (c->t.param_bf16) {
         if (gck::launch_cast_bf16(c->t.master, c->t.param_bf16, c->cfg.n, stream, c->num_sms))
             return c->cuda_fail(cudaGetLastError(), "restore bf16 cast");

@@ -7,6 +7,7 @@
 #include <cstddef>
 #include <cstdint>
 #include <string>
+#include <vector>
 
 #include "gockpt.h"
 
@@ -53,11 +54,37 @@ int launch_generate(int kind, int mode, uint64_t seed, uint64_t step, uint64_t o
 int launch_cast_bf16(const float *src, uint16_t *dst, uint64_t n, void *stream, int num_sms);
 
 // Persistence (persist.cpp).
+// The replay log a version-2 (replay-on-restore) file carries: the session plan, its K
+// StepRecords and the host gradient slices glog[i] (hi[i] elements, i < K-1).
+struct ReplayLog {
+    uint32_t K = 0;
+    uint64_t t0 = 0;
+    uint64_t lo[GCK_K_LIMIT]{}, hi[GCK_K_LIMIT]{};
+    gck_step_record rec[GCK_K_LIMIT]{};
+    const uint16_t *glog[GCK_K_LIMIT]{};
+};
+// A version-2 load that defers the replay to the caller (the GPU restore) receives the log
+// here; the slices land in `buf` (buf_elems capacity, slices 128-element aligned) if it is
+// large enough, else in `storage`.
+struct LoadedLog {
+    bool present = false;
+    gck_log_header lh{};
+    uint16_t *glog[GCK_K_LIMIT]{};
+    uint16_t *buf = nullptr;
+    uint64_t buf_elems = 0;
+    std::vector<uint16_t> storage;
+};
+// Checks a plan (contiguous, ascending, non-empty parts covering [0, n)); "" if valid.
+std::string plan_error(uint32_t K, const uint64_t *lo, const uint64_t *hi, uint64_t n);
+
 gck_status write_checkpoint_impl(const char *path, const gck_file_header *hdr, const float *const sec[3], int threads,
-                                 const char *meta_json, gck_persist_stats *stats, std::string *err);
+                                 const char *meta_json, gck_persist_stats *stats, std::string *err,
+                                 const ReplayLog *log = nullptr);
 gck_status read_header_impl(const char *path, gck_file_header *out, std::string *err);
+gck_status read_log_header_impl(const char *path, gck_log_header *out, std::string *err);
+// defer == nullptr: a version-2 file is replayed on the host (threads) after the read.
 gck_status load_checkpoint_impl(const char *path, float *const dst[3], uint64_t n, int threads, gck_file_header *hdr_out,
-                                gck_persist_stats *stats, std::string *err);
+                                gck_persist_stats *stats, std::string *err, LoadedLog *defer = nullptr);
 
 gck_status load_range_impl(const char *path, uint64_t offset, uint64_t count, float *const dst[3], int threads,
                            gck_file_header *hdr_out, std::string *err);

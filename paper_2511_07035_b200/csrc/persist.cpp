@@ -62,6 +62,33 @@ Layout layout_for(uint64_t n) {
     return L;
 }
 
+// Version 2 (replay-on-restore): the replay log follows the version-1 layout of the same n.
+struct LogLayout {
+    uint64_t log_off, table_off, table_bytes, nblocks, file_bytes;
+    uint64_t slice_off[GCK_K_LIMIT], slice_bytes[GCK_K_LIMIT], slice_block0[GCK_K_LIMIT];
+};
+
+LogLayout log_layout_for(const Layout &L, uint32_t K, const uint64_t *hi) {
+    LogLayout G{};
+    G.log_off = L.file_bytes;
+    G.table_off = G.log_off + GCK_LOG_HEADER_BYTES;
+    for (uint32_t i = 0; i + 1 < K; ++i) {
+        G.slice_bytes[i] = hi[i] * 2;
+        G.slice_block0[i] = G.nblocks;
+        G.nblocks += (G.slice_bytes[i] + kBlock - 1) / kBlock;
+    }
+    G.table_bytes = align_up(G.nblocks * 4, kPage);
+    uint64_t off = G.table_off + G.table_bytes;
+    for (uint32_t i = 0; i + 1 < K; ++i) {
+        G.slice_off[i] = off;
+        off = align_up(off + G.slice_bytes[i], kPage);
+    }
+    G.file_bytes = off;
+    return G;
+}
+
+static_assert(sizeof(gck_log_header) <= GCK_LOG_HEADER_BYTES, "log header page");
+
 bool pwrite_all(int fd, const void *buf, uint64_t len, uint64_t off) {
     const char *p = static_cast<const char *>(buf);
     while (len) {
@@ -141,7 +168,8 @@ long fault_after_blocks() {
 }  // namespace
 
 gck_status write_checkpoint_impl(const char *path, const gck_file_header *hdr_in, const float *const sec[3],
-                                 int threads, const char *meta_json, gck_persist_stats *stats, std::string *err) {
+                                 int threads, const char *meta_json, gck_persist_stats *stats, std::string *err,
+                                 const ReplayLog *log) {
     const auto t0 = std::chrono::steady_clock::now();
     if (!path || !hdr_in || !sec[0] || !sec[1] || !sec[2]) {
         *err = "null argument";
@@ -149,19 +177,28 @@ gck_status write_checkpoint_impl(const char *path, const gck_file_header *hdr_in
     }
     const uint64_t n = hdr_in->n;
     const Layout L = layout_for(n);
+    LogLayout G{};
+    if (log) G = log_layout_for(L, log->K, log->hi);
+    const uint64_t file_bytes = log ? G.file_bytes : L.file_bytes;
     const std::string final_path(path), tmp = final_path + ".tmp";
     const int fd = ::open(tmp.c_str(), O_CREAT | O_TRUNC | O_WRONLY, 0644);
     if (fd < 0) {
         *err = "open " + tmp + ": " + strerror(errno);
         return GCK_E_IO;
     }
-    if (::ftruncate(fd, (off_t)L.file_bytes) != 0) {
+    if (::ftruncate(fd, (off_t)file_bytes) != 0) {
         *err = std::string("ftruncate: ") + strerror(errno);
         ::close(fd);
         return GCK_E_IO;
     }
-    std::vector<uint32_t> table(3 * L.nblocks, 0);
-    const uint64_t total = 3 * L.nblocks;
+    // jobs [0, 3 nblocks): state blocks (CRC -> table); then the gradient-slice blocks (-> gtable)
+    std::vector<uint32_t> table(3 * L.nblocks, 0), gtable(G.nblocks, 0);
+    std::vector<uint32_t> gslice(G.nblocks);  // slice of each gradient block
+    if (log)
+        for (uint32_t i = 0; i + 1 < log->K; ++i)
+            for (uint64_t b = G.slice_block0[i]; b < G.slice_block0[i] + (G.slice_bytes[i] + kBlock - 1) / kBlock; ++b)
+                gslice[b] = i;
+    const uint64_t total = 3 * L.nblocks + G.nblocks;
     std::atomic<uint64_t> next{0};
     std::atomic<bool> failed{false};
     const long fault = fault_after_blocks();
@@ -173,12 +210,21 @@ gck_status write_checkpoint_impl(const char *path, const gck_file_header *hdr_in
                 failed = true;
                 break;
             }
-            const int s = (int)(j / L.nblocks);
-            const uint64_t b = j % L.nblocks;
-            const uint64_t off = b * kBlock, len = std::min(kBlock, L.sec_bytes - off);
-            const char *src = reinterpret_cast<const char *>(sec[s]) + off;
-            table[j] = crc32_of(src, len);
-            if (!pwrite_all(fd, src, len, L.sec_off[s] + off)) failed = true;
+            if (j < 3 * L.nblocks) {
+                const int s = (int)(j / L.nblocks);
+                const uint64_t b = j % L.nblocks;
+                const uint64_t off = b * kBlock, len = std::min(kBlock, L.sec_bytes - off);
+                const char *src = reinterpret_cast<const char *>(sec[s]) + off;
+                table[j] = crc32_of(src, len);
+                if (!pwrite_all(fd, src, len, L.sec_off[s] + off)) failed = true;
+            } else {
+                const uint64_t gb = j - 3 * L.nblocks;
+                const uint32_t i = gslice[gb];
+                const uint64_t off = (gb - G.slice_block0[i]) * kBlock, len = std::min(kBlock, G.slice_bytes[i] - off);
+                const char *src = reinterpret_cast<const char *>(log->glog[i]) + off;
+                gtable[gb] = crc32_of(src, len);
+                if (!pwrite_all(fd, src, len, G.slice_off[i] + off)) failed = true;
+            }
         }
     };
     if (threads <= 0) threads = std::min(16, default_threads());
@@ -197,7 +243,7 @@ gck_status write_checkpoint_impl(const char *path, const gck_file_header *hdr_in
     std::memcpy(tbl.data(), table.data(), table.size() * 4);
     gck_file_header h = *hdr_in;
     std::memcpy(h.magic, GCK_FILE_MAGIC, 8);
-    h.version = GCK_FILE_VERSION;
+    h.version = log ? GCK_FILE_VERSION_LOG : GCK_FILE_VERSION;
     h.header_bytes = (uint32_t)kPage;
     h.block_bytes = kBlock;
     h.nblocks = L.nblocks;
@@ -211,7 +257,30 @@ gck_status write_checkpoint_impl(const char *path, const gck_file_header *hdr_in
     h.header_crc = crc32_of(&h, offsetof(gck_file_header, header_crc));
     std::vector<char> page(kPage, 0);
     std::memcpy(page.data(), &h, sizeof(h));
-    bool ok = pwrite_all(fd, tbl.data(), tbl.size(), L.table_off) && pwrite_all(fd, page.data(), kPage, 0);
+    bool ok = pwrite_all(fd, tbl.data(), tbl.size(), L.table_off);
+    if (log && ok) {  // the replay log header + gradient CRC table, before the file header
+        std::vector<char> gt(G.table_bytes, 0);
+        std::memcpy(gt.data(), gtable.data(), gtable.size() * 4);
+        gck_log_header lh;
+        std::memset(&lh, 0, sizeof(lh));
+        std::memcpy(lh.magic, GCK_LOG_MAGIC, 8);
+        lh.K = log->K;
+        lh.t0 = log->t0;
+        for (uint32_t i = 0; i < log->K; ++i) {
+            lh.lo[i] = log->lo[i];
+            lh.hi[i] = log->hi[i];
+            lh.rec[i] = log->rec[i];
+            lh.glog_offset[i] = (i + 1 < log->K) ? G.slice_off[i] : 0;
+        }
+        lh.glog_table_offset = G.table_off;
+        lh.glog_nblocks = G.nblocks;
+        lh.glog_table_crc = crc32_of(gtable.data(), gtable.size() * 4);
+        lh.log_crc = crc32_of(&lh, offsetof(gck_log_header, log_crc));
+        std::vector<char> lpage(GCK_LOG_HEADER_BYTES, 0);
+        std::memcpy(lpage.data(), &lh, sizeof(lh));
+        ok = pwrite_all(fd, gt.data(), gt.size(), G.table_off) && pwrite_all(fd, lpage.data(), lpage.size(), G.log_off);
+    }
+    ok = ok && pwrite_all(fd, page.data(), kPage, 0);
     const auto t_data = std::chrono::steady_clock::now();
     ok = ok && ::fsync(fd) == 0;
     ok = (::close(fd) == 0) && ok;
@@ -228,10 +297,10 @@ gck_status write_checkpoint_impl(const char *path, const gck_file_header *hdr_in
     // metadata callback, then the LATEST pointer: the checkpoint is complete from here on
     char meta[1024];
     snprintf(meta, sizeof(meta),
-             "{\"file\": \"%s\", \"step\": %llu, \"adam_t\": %llu, \"n\": %llu, \"rank\": %u, \"world\": %u, "
-             "\"bytes\": %llu, \"user\": %s}\n",
-             base_of(final_path).c_str(), (unsigned long long)h.step, (unsigned long long)h.adam_t,
-             (unsigned long long)n, h.rank, h.world, (unsigned long long)L.file_bytes,
+             "{\"file\": \"%s\", \"version\": %u, \"step\": %llu, \"adam_t\": %llu, \"n\": %llu, \"rank\": %u, "
+             "\"world\": %u, \"bytes\": %llu, \"user\": %s}\n",
+             base_of(final_path).c_str(), h.version, (unsigned long long)h.step, (unsigned long long)h.adam_t,
+             (unsigned long long)n, h.rank, h.world, (unsigned long long)file_bytes,
              meta_json && *meta_json ? meta_json : "null");
     if (!write_small_file_atomic(final_path + ".meta.json", meta) ||
         !write_small_file_atomic(dir + "/LATEST.rank" + std::to_string(h.rank), base_of(final_path) + "\n")) {
@@ -241,7 +310,7 @@ gck_status write_checkpoint_impl(const char *path, const gck_file_header *hdr_in
     fsync_dir(dir);
     const auto t1 = std::chrono::steady_clock::now();
     if (stats) {
-        stats->bytes = L.file_bytes;
+        stats->bytes = file_bytes;
         stats->threads = threads;
         stats->seconds = std::chrono::duration<double>(t1 - t0).count();
         stats->data_seconds = std::chrono::duration<double>(t_data - t0).count();
@@ -265,7 +334,8 @@ gck_status read_header_impl(const char *path, gck_file_header *out, std::string 
     }
     gck_file_header h;
     std::memcpy(&h, page.data(), sizeof(h));
-    if (std::memcmp(h.magic, GCK_FILE_MAGIC, 8) != 0 || h.version != GCK_FILE_VERSION) {
+    if (std::memcmp(h.magic, GCK_FILE_MAGIC, 8) != 0 ||
+        (h.version != GCK_FILE_VERSION && h.version != GCK_FILE_VERSION_LOG)) {
         *err = "not a GoCkpt checkpoint file (magic/version)";
         return GCK_E_CORRUPT;
     }
@@ -277,8 +347,88 @@ gck_status read_header_impl(const char *path, gck_file_header *out, std::string 
     return GCK_OK;
 }
 
+std::string plan_error(uint32_t K, const uint64_t *lo, const uint64_t *hi, uint64_t n) {
+    if (K < 1 || K > GCK_K_LIMIT) return "K outside 1..64";
+    for (uint32_t i = 0; i < K; ++i) {
+        if (lo[i] != (i ? hi[i - 1] : 0)) return "parts are not contiguous from 0";
+        if (hi[i] <= lo[i]) return "empty part";
+    }
+    if (hi[K - 1] != n) return "parts do not cover [0, n)";
+    return "";
+}
+
+namespace {
+
+// Read + validate the replay log header of a version-2 file (fd open), and its layout.
+gck_status read_log(int fd, const gck_file_header &h, gck_log_header *lh, LogLayout *G, std::string *err) {
+    const Layout L = layout_for(h.n);
+    std::vector<char> page(GCK_LOG_HEADER_BYTES);
+    if (!pread_all(fd, page.data(), page.size(), L.file_bytes)) {
+        *err = "version-2 file shorter than its replay log header";
+        return GCK_E_CORRUPT;
+    }
+    std::memcpy(lh, page.data(), sizeof(*lh));
+    if (std::memcmp(lh->magic, GCK_LOG_MAGIC, 8) != 0) {
+        *err = "replay log magic mismatch";
+        return GCK_E_CORRUPT;
+    }
+    if (crc32_of(lh, offsetof(gck_log_header, log_crc)) != lh->log_crc) {
+        *err = "replay log header CRC mismatch";
+        return GCK_E_CORRUPT;
+    }
+    const std::string pe = plan_error(lh->K, lh->lo, lh->hi, h.n);
+    if (!pe.empty()) {
+        *err = "replay log plan: " + pe;
+        return GCK_E_CORRUPT;
+    }
+    if (lh->t0 + lh->K - 1 != h.step) {
+        *err = "replay log t0 + K - 1 != header step";
+        return GCK_E_CORRUPT;
+    }
+    *G = log_layout_for(L, lh->K, lh->hi);
+    bool same = G->table_off == lh->glog_table_offset && G->nblocks == lh->glog_nblocks;
+    for (uint32_t i = 0; i + 1 < lh->K; ++i) same = same && G->slice_off[i] == lh->glog_offset[i];
+    if (!same) {
+        *err = "replay log layout fields inconsistent with the plan";
+        return GCK_E_CORRUPT;
+    }
+    return GCK_OK;
+}
+
+gck_status read_gtable(int fd, const gck_log_header &lh, std::vector<uint32_t> *gtable, std::string *err) {
+    gtable->assign(lh.glog_nblocks, 0);
+    if (!pread_all(fd, gtable->data(), gtable->size() * 4, lh.glog_table_offset) ||
+        crc32_of(gtable->data(), gtable->size() * 4) != lh.glog_table_crc) {
+        *err = "gradient CRC table unreadable or corrupt";
+        return GCK_E_CORRUPT;
+    }
+    return GCK_OK;
+}
+
+}  // namespace
+
+gck_status read_log_header_impl(const char *path, gck_log_header *out, std::string *err) {
+    gck_file_header h;
+    gck_status st = read_header_impl(path, &h, err);
+    if (st != GCK_OK) return st;
+    if (h.version != GCK_FILE_VERSION_LOG) {
+        *err = "not a replay-on-restore (version 2) file";
+        return GCK_E_INVALID;
+    }
+    const int fd = ::open(path, O_RDONLY);
+    if (fd < 0) {
+        *err = std::string("open: ") + strerror(errno);
+        return GCK_E_IO;
+    }
+    LogLayout G;
+    st = read_log(fd, h, out, &G, err);
+    ::close(fd);
+    return st;
+}
+
 gck_status load_checkpoint_impl(const char *path, float *const dst[3], uint64_t n, int threads,
-                                gck_file_header *hdr_out, gck_persist_stats *stats, std::string *err) {
+                                gck_file_header *hdr_out, gck_persist_stats *stats, std::string *err,
+                                LoadedLog *defer) {
     const auto t0 = std::chrono::steady_clock::now();
     gck_file_header h;
     gck_status st = read_header_impl(path, &h, err);
@@ -304,7 +454,38 @@ gck_status load_checkpoint_impl(const char *path, float *const dst[3], uint64_t 
         *err = "CRC table unreadable or corrupt";
         return GCK_E_CORRUPT;
     }
-    const uint64_t total = 3 * L.nblocks;
+    // version 2: the replay log, its gradient slices read with the state blocks
+    gck_log_header lh{};
+    LogLayout G{};
+    std::vector<uint32_t> gtable, gslice;
+    LoadedLog local;
+    LoadedLog *lg = defer ? defer : &local;
+    if (h.version == GCK_FILE_VERSION_LOG) {
+        if ((st = read_log(fd, h, &lh, &G, err)) != GCK_OK || (st = read_gtable(fd, lh, &gtable, err)) != GCK_OK) {
+            ::close(fd);
+            return st;
+        }
+        uint64_t need = 0, offs[GCK_K_LIMIT] = {};
+        for (uint32_t i = 0; i + 1 < lh.K; ++i) {
+            offs[i] = need;
+            need += align_up(lh.hi[i], 128);
+        }
+        uint16_t *base = nullptr;
+        if (lg->buf && lg->buf_elems >= need) {
+            base = lg->buf;
+        } else {
+            lg->storage.assign(need, 0);
+            base = lg->storage.data();
+        }
+        lg->present = true;
+        lg->lh = lh;
+        for (uint32_t i = 0; i + 1 < lh.K; ++i) lg->glog[i] = base + offs[i];
+        gslice.assign(G.nblocks, 0);
+        for (uint32_t i = 0; i + 1 < lh.K; ++i)
+            for (uint64_t b = G.slice_block0[i]; b < G.slice_block0[i] + (G.slice_bytes[i] + kBlock - 1) / kBlock; ++b)
+                gslice[b] = i;
+    }
+    const uint64_t total = 3 * L.nblocks + G.nblocks;
     std::atomic<uint64_t> next{0};
     std::atomic<int> bad{0};  // 1 = io, 2 = crc
     std::atomic<uint64_t> bad_block{0};
@@ -312,15 +493,31 @@ gck_status load_checkpoint_impl(const char *path, float *const dst[3], uint64_t 
         for (;;) {
             const uint64_t j = next.fetch_add(1);
             if (j >= total || bad.load()) break;
-            const int s = (int)(j / L.nblocks);
-            const uint64_t b = j % L.nblocks;
-            const uint64_t off = b * kBlock, len = std::min(kBlock, L.sec_bytes - off);
-            char *p = reinterpret_cast<char *>(dst[s]) + off;
-            if (!pread_all(fd, p, len, L.sec_off[s] + off)) {
+            char *p;
+            uint64_t len, foff;
+            uint32_t want;
+            if (j < 3 * L.nblocks) {
+                const int s = (int)(j / L.nblocks);
+                const uint64_t b = j % L.nblocks;
+                const uint64_t off = b * kBlock;
+                len = std::min(kBlock, L.sec_bytes - off);
+                p = reinterpret_cast<char *>(dst[s]) + off;
+                foff = L.sec_off[s] + off;
+                want = table[j];
+            } else {
+                const uint64_t gb = j - 3 * L.nblocks;
+                const uint32_t i = gslice[gb];
+                const uint64_t off = (gb - G.slice_block0[i]) * kBlock;
+                len = std::min(kBlock, G.slice_bytes[i] - off);
+                p = reinterpret_cast<char *>(lg->glog[i]) + off;
+                foff = G.slice_off[i] + off;
+                want = gtable[gb];
+            }
+            if (!pread_all(fd, p, len, foff)) {
                 bad = 1;
                 break;
             }
-            if (crc32_of(p, len) != table[j]) {
+            if (crc32_of(p, len) != want) {
                 bad_block = j;
                 bad = 2;
                 break;
@@ -342,10 +539,19 @@ gck_status load_checkpoint_impl(const char *path, float *const dst[3], uint64_t 
         *err = "data CRC mismatch in block " + std::to_string(bad_block.load());
         return GCK_E_CORRUPT;
     }
+    if (h.version == GCK_FILE_VERSION_LOG && !defer) {  // replay on the host: parts j < K to S(T)
+        const uint16_t *gl[GCK_K_LIMIT] = {};
+        for (uint32_t i = 0; i + 1 < lh.K; ++i) gl[i] = lg->glog[i];
+        st = replay_host_impl(lh.rec, lh.K, lh.lo, lh.hi, dst[0], dst[1], dst[2], gl, threads, nullptr);
+        if (st != GCK_OK) {
+            *err = "host replay of the loaded log failed";
+            return st;
+        }
+    }
     if (hdr_out) *hdr_out = h;
     if (stats) {
         const auto t1 = std::chrono::steady_clock::now();
-        stats->bytes = L.file_bytes;
+        stats->bytes = h.version == GCK_FILE_VERSION_LOG ? G.file_bytes : L.file_bytes;
         stats->threads = threads;
         stats->seconds = std::chrono::duration<double>(t1 - t0).count();
         stats->data_seconds = stats->seconds;
@@ -416,11 +622,52 @@ gck_status load_range_impl(const char *path, uint64_t offset, uint64_t count, fl
     for (int k = 1; k < threads; ++k) pool.emplace_back(worker);
     worker();
     for (auto &t : pool) t.join();
-    ::close(fd);
     if (bad) {
+        ::close(fd);
         *err = bad == 1 ? "truncated or unreadable data section" : "data CRC mismatch in a touched block";
         return GCK_E_CORRUPT;
     }
+    if (h.version == GCK_FILE_VERSION_LOG) {
+        // the gradient slices over [offset, end), every touched block CRC-verified, then the
+        // replay of the range: the update is elementwise, so a range replays on its own
+        gck_log_header lh;
+        LogLayout G;
+        std::vector<uint32_t> gtable;
+        if ((st = read_log(fd, h, &lh, &G, err)) != GCK_OK || (st = read_gtable(fd, lh, &gtable, err)) != GCK_OK) {
+            ::close(fd);
+            return st;
+        }
+        const uint64_t end = offset + count;
+        std::vector<std::vector<uint16_t>> bufs(lh.K);
+        const uint16_t *gl[GCK_K_LIMIT] = {};
+        uint64_t rlo[GCK_K_LIMIT], rhi[GCK_K_LIMIT];
+        std::vector<char> blk;
+        for (uint32_t i = 0; i < lh.K; ++i) {
+            rlo[i] = std::min(std::max(lh.lo[i], offset), end) - offset;
+            rhi[i] = std::min(std::max(lh.hi[i], offset), end) - offset;
+            if (i + 1 == lh.K) break;
+            bufs[i].assign(count, 0);
+            gl[i] = bufs[i].data();
+            const uint64_t e1 = std::min(end, lh.hi[i]);  // slice i holds [0, hi_i)
+            if (e1 <= offset) continue;
+            const uint64_t bb0 = offset * 2 / kBlock, bb1 = (e1 * 2 + kBlock - 1) / kBlock;
+            for (uint64_t b = bb0; b < bb1; ++b) {
+                const uint64_t off = b * kBlock, len = std::min(kBlock, G.slice_bytes[i] - off);
+                blk.resize(len);
+                if (!pread_all(fd, blk.data(), len, G.slice_off[i] + off) ||
+                    crc32_of(blk.data(), len) != gtable[G.slice_block0[i] + b]) {
+                    ::close(fd);
+                    *err = "gradient slice unreadable or CRC mismatch in a touched block";
+                    return GCK_E_CORRUPT;
+                }
+                const uint64_t a = std::max(off, offset * 2), z = std::min(off + len, e1 * 2);
+                std::memcpy(reinterpret_cast<char *>(bufs[i].data()) + (a - offset * 2), blk.data() + (a - off), z - a);
+            }
+        }
+        ::close(fd);
+        return replay_host_impl(lh.rec, lh.K, rlo, rhi, dst[0], dst[1], dst[2], gl, threads, nullptr);
+    }
+    ::close(fd);
     return GCK_OK;
 }
 

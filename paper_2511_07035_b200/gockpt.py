@@ -131,10 +131,41 @@ def write_checkpoint(path: str, master: np.ndarray, m: np.ndarray, v: np.ndarray
     return st.as_dict()
 
 
+def write_checkpoint_log(path: str, master: np.ndarray, m: np.ndarray, v: np.ndarray, *, t0: int, parts, recs,
+                         glog, adam_t: int, rank: int = 0, world: int = 1, beta1=0.9, beta2=0.999, eps=1e-8,
+                         weight_decay=0.01, threads: int = 0, meta_json: str | None = None) -> dict:
+    """NEXT-2 replay-on-restore (gck_write_checkpoint_log): a version-2 file of the captured parts
+    (part i at S(t0+i-1)), the K StepRecords and the gradient slices glog[i-1] (hi_i uint16 each)."""
+    K = len(parts)
+    h = L.FileHeader()
+    h.step, h.adam_t, h.n, h.rank, h.world = t0 + K - 1, adam_t, len(master), rank, world
+    h.beta1, h.beta2, h.eps, h.weight_decay = beta1, beta2, eps, weight_decay
+    gl = (C.c_void_p * max(1, K))()
+    for i, g in enumerate(glog):
+        gl[i] = _host_ptr(g, np.uint16)
+    st = L.PersistStats()
+    check(lib().gck_write_checkpoint_log(path.encode(), C.byref(h), _host_ptr(master, np.float32),
+                                         _host_ptr(m, np.float32), _host_ptr(v, np.float32), K, t0,
+                                         _parts_array(parts), _recs_array(recs), gl, threads,
+                                         meta_json.encode() if meta_json else None, C.byref(st)))
+    return st.as_dict()
+
+
 def read_header(path: str) -> dict:
     h = L.FileHeader()
     check(lib().gck_read_header(path.encode(), C.byref(h)))
-    return _hdr_dict(h)
+    d = _hdr_dict(h)
+    d["version"] = h.version
+    return d
+
+
+def read_log_header(path: str) -> dict:
+    """The replay log of a version-2 file: t0, K, parts, StepRecords, slice offsets."""
+    lh = L.LogHeader()
+    check(lib().gck_read_log_header(path.encode(), C.byref(lh)))
+    K = lh.K
+    return dict(t0=lh.t0, K=K, parts=[(lh.lo[i], lh.hi[i]) for i in range(K)], recs=[lh.rec[i] for i in range(K)],
+                glog_offset=[lh.glog_offset[i] for i in range(K - 1)], glog_nblocks=lh.glog_nblocks)
 
 
 def load_checkpoint(path: str, n: int, threads: int = 0):
@@ -189,6 +220,8 @@ class HostCheckpoint:
     master: np.ndarray
     exp_avg: np.ndarray
     exp_avg_sq: np.ndarray
+    K: int = 0
+    replay_pending: bool = False  # replay_mode="deferred": parts still as captured; S(T) at load
 
 
 class GoCkpt:
@@ -205,7 +238,8 @@ class GoCkpt:
         self._keep = (master, exp_avg, exp_avg_sq, param_bf16)
         cfg = L.Config(L.ABI_VERSION, master.device.index or 0, n, k_min, k_max, part_align, ring_slots,
                        {"ce": L.COPY_ENGINE, "zerocopy": L.COPY_ZEROCOPY}[copy_mode], chunk_bytes, zc_ctas,
-                       {"host": L.REPLAY_HOST, "gpu": L.REPLAY_GPU}[replay_mode], replay_threads, int(timing),
+                       {"host": L.REPLAY_HOST, "gpu": L.REPLAY_GPU, "deferred": L.REPLAY_DEFERRED}[replay_mode],
+                       replay_threads, int(timing),
                        int(eager_replay),
                        {"ring": L.STAGE_RING, "direct": L.STAGE_DIRECT, "blocking": L.STAGE_BLOCKING}[staging],
                        numa_node)
@@ -256,7 +290,8 @@ class GoCkpt:
             return None
         check(st, self._ctx)
         return HostCheckpoint(ck.step, _np_view(ck.master, ck.n, np.float32),
-                              _np_view(ck.exp_avg, ck.n, np.float32), _np_view(ck.exp_avg_sq, ck.n, np.float32))
+                              _np_view(ck.exp_avg, ck.n, np.float32), _np_view(ck.exp_avg_sq, ck.n, np.float32),
+                              ck.K, bool(ck.replay_pending))
 
     def release(self):
         check(lib().gck_release(self._ctx), self._ctx)

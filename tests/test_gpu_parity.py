@@ -279,10 +279,14 @@ def test_d2h_copy_byte_exact(G, nbytes, mode, chunk, ctas):
 
 
 # ---------------------------------------------------------------- NEXT-1: persist + crash + restore + resume
-def test_persist_restore_resume_equals_uninterrupted(G, tmp_path):
+@pytest.mark.parametrize("replay_mode,k_max2", [("host", 4), ("deferred", 4), ("deferred", 2)])
+def test_persist_restore_resume_equals_uninterrupted(G, tmp_path, replay_mode, k_max2):
     """SPEC S:506 recovery correctness: train, checkpoint (GoCkpt session), persist in the
     background, keep training, 'crash', restore from LATEST into a fresh context, resume at T+1
-    with the same gradients -> bit-identical to the run that never crashed."""
+    with the same gradients -> bit-identical to the run that never crashed. replay_mode
+    "deferred" (replay-on-restore, NEXT-2): the file carries the captured parts + gradient log and
+    the restore replays on the GPU (k_max2 = 2 < K: the log does not fit the restoring context's
+    arena and goes through a temporary buffer)."""
     from oracle import ckpt_file as OF
     n, K, seed = 300_007, 4, 21
     state = gi.warm_state(seed, n)
@@ -307,10 +311,10 @@ def test_persist_restore_resume_equals_uninterrupted(G, tmp_path):
     ref.close()
     # run with a checkpoint over steps 6..9 (T = 8), persisted while training continues to 13
     p, m, v = (up_f32(x) for x in state)
-    ctx = G.GoCkpt(p, m, v, None, **HP, k_min=K, k_max=K, part_align=64)
+    ctx = G.GoCkpt(p, m, v, None, **HP, k_min=K, k_max=K, part_align=64, replay_mode=replay_mode)
     train(ctx, range(1, 10), begin_at=5)
     ck = ctx.finalize()
-    assert ck.step == 8
+    assert ck.step == 8 and ck.K == K and ck.replay_pending == (replay_mode == "deferred")
     path = str(tmp_path / "ckpt_8.rank0.bin")
     ctx.persist_begin(path, 0, 1, '{"note": "test"}')
     train(ctx, range(10, 14))
@@ -318,19 +322,71 @@ def test_persist_restore_resume_equals_uninterrupted(G, tmp_path):
     assert st["bytes"] > 12 * n
     ctx.release()
     ctx.close()                                                   # the crash
-    hdr, *_ = OF.read(OF.latest(str(tmp_path)))                    # the independent reader agrees
+    hdr, *s8 = OF.read_consistent(OF.latest(str(tmp_path)))      # the independent reader (+ oracle replay)
     assert hdr["step"] == 8 and hdr["adam_t"] == 8
+    assert hdr.get("version", 1) == (2 if replay_mode == "deferred" else 1)
+    recs8 = [oracle.make_step_record(t=s, lr=1e-3, **HP) for s in range(1, 9)]
+    assert_state_equal(tuple(s8), oracle.trajectory(*state, grads[:8], recs8)[-1], "file vs oracle S(8)")
     # fresh process state: garbage tensors, restore, resume at T+1 = 9
     p2, m2, v2 = (torch.full((n,), 7.0, device="cuda") for _ in range(3))
     out = torch.zeros(n, dtype=torch.int16, device="cuda")
-    ctx2 = G.GoCkpt(p2, m2, v2, out, **HP, k_min=K, k_max=K, part_align=64)
+    ctx2 = G.GoCkpt(p2, m2, v2, out, **HP, k_min=1, k_max=k_max2, part_align=64)
     h = ctx2.restore(OF.latest(str(tmp_path)))
     assert h["step"] == 8
+    torch.cuda.synchronize()
+    assert_state_equal((down_f32(p2), down_f32(m2), down_f32(v2)), tuple(s8), "restored S(8)")
     assert np.array_equal(down_u16(out), oracle.rne_bf16(down_f32(p2)))   # working copy re-derived
     train(ctx2, range(h["step"] + 1, total + 1))
     torch.cuda.synchronize()
     assert_state_equal((down_f32(p2), down_f32(m2), down_f32(v2)), want, "resumed vs uninterrupted")
     ctx2.close()
+
+
+# ---------------------------------------------------------------- NEXT-2: replay-on-restore
+@pytest.mark.parametrize("n,K,A,staging", [(1 << 20, 4, 1024, "ring"), (1_000_003, 8, 1024, "ring"),
+                                           (300_007, 3, 8, "direct"), (5000, 1, 8, "ring"),
+                                           ((1 << 18) + 4101, 16, 1024, "ring")])
+def test_deferred_replay_session_restore(G, tmp_path, n, K, A, staging):
+    """replay_mode="deferred": finalize leaves the captured parts (== the oracle's capture, bit for
+    bit), persist writes them with the gradient log, and the GPU restore (replay kernel in place on
+    the device tensors) and the host loader both give the oracle's S(T) bit for bit."""
+    t0, seed = 10, 13
+    state, grads, recs, sargs = session_inputs(seed, n, K, t0, skips=(t0 + 2,) if K >= 3 else ())
+    ctx, (p, m, v, out) = _make_ctx(G, state, K, part_align=A, staging=staging, replay_mode="deferred")
+    parts = oracle.make_parts(n, K, A)
+    cap, glog, live = oracle.capture_session(*state, grads, recs, parts)
+    want = oracle.trajectory(*state, grads[:K - 1], recs[:K - 1])[-1]
+    ctx.begin_checkpoint(t0, K)
+    gbuf = None
+    for i in range(1, K + 1):
+        a = sargs[i - 1]
+        if staging == "direct":
+            if gbuf is None:
+                gbuf = up_u16(grads[i - 1])
+            else:
+                gbuf.copy_(up_u16(grads[i - 1]))
+            ctx.submit(i, a["step"], a["adam_t"], a["lr"], gbuf, a["grad_scale"], a["skip"])
+            ctx.grad_fence()
+        else:
+            ctx.submit(i, a["step"], a["adam_t"], a["lr"], up_u16(grads[i - 1]), a["grad_scale"], a["skip"])
+    ck = ctx.finalize()
+    assert ck.step == t0 + K - 1 and ck.replay_pending == (K > 1)
+    assert_state_equal((ck.master, ck.exp_avg, ck.exp_avg_sq), oracle.assemble(cap), "captured parts")
+    path = str(tmp_path / "d.bin")
+    ctx.persist_begin(path)
+    ctx.persist_wait()
+    ctx.release()
+    torch.cuda.synchronize()
+    assert_state_equal((down_f32(p), down_f32(m), down_f32(v)), live, "live S(t0+K)")
+    hp_, hm_, hv_, hdr, _ = G.load_checkpoint(path, n, threads=4)            # host replay at load
+    assert hdr["step"] == t0 + K - 1
+    assert_state_equal((hp_, hm_, hv_), want, "host-loaded S(T)")
+    h = ctx.restore(path)                                                   # GPU replay at restore
+    torch.cuda.synchronize()
+    assert h["step"] == t0 + K - 1
+    assert_state_equal((down_f32(p), down_f32(m), down_f32(v)), want, "GPU-restored S(T)")
+    assert np.array_equal(down_u16(out), oracle.rne_bf16(want[0]))
+    ctx.close()
 
 
 # ---------------------------------------------------------------- NEXT-2: direct staging (GoCkpt-O literal)
