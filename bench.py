@@ -77,8 +77,10 @@ def parse():
                     help="NEXT-3 baselines in the same harness: sync = blocking D2H snapshot of the full "
                          "state (DeepSpeed/Async snapshot phase); async-o = the snapshot overlaps the next "
                          "step's F/B and its update waits for it (P:312-318)")
-    ap.add_argument("--replay-mode", default="host", choices=["host", "gpu"],
-                    help="consistency replay on the host pool (default) or in the GPU replay kernel")
+    ap.add_argument("--replay-mode", default="host", choices=["host", "gpu", "deferred"],
+                    help="consistency replay on the host pool (default) or in the GPU replay kernel; deferred "
+                         "= replay-on-restore (finalize leaves the captured parts + gradient log for the "
+                         "persisted file; S(T) is materialised at load)")
     ap.add_argument("--replay-threads", type=int, default=0,
                     help="host replay / persist threads (0 = the host's cores divided by the local ranks)")
     ap.add_argument("--no-e2e", action="store_true")
