@@ -77,10 +77,12 @@ def parse():
                     help="NEXT-3 baselines in the same harness: sync = blocking D2H snapshot of the full "
                          "state (DeepSpeed/Async snapshot phase); async-o = the snapshot overlaps the next "
                          "step's F/B and its update waits for it (P:312-318)")
-    ap.add_argument("--replay-mode", default="host", choices=["host", "gpu", "deferred"],
+    ap.add_argument("--replay-mode", default="host", choices=["host", "gpu", "deferred", "stream"],
                     help="consistency replay on the host pool (default) or in the GPU replay kernel; deferred "
                          "= replay-on-restore (finalize leaves the captured parts + gradient log for the "
-                         "persisted file; S(T) is materialised at load)")
+                         "persisted file; S(T) is materialised at load); stream = streaming host replay (each slice's "
+                         "update applied as it drains; gradient log = --stream-buffers recycled slices)")
+    ap.add_argument("--stream-buffers", type=int, default=0, help="streaming replay slice buffers (0 = 2)")
     ap.add_argument("--replay-threads", type=int, default=0,
                     help="host replay / persist threads (0 = the host's cores divided by the local ranks)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -239,7 +241,8 @@ def main():
     ctx = G.GoCkpt(master, exp_avg, exp_avg_sq, param, **HP, k_min=1 if auto_k else K, k_max=32 if auto_k else K,
                    part_align=1024,
                    ring_slots=args.ring_slots, copy_mode=args.copy_mode, replay_threads=args.replay_threads,
-                   timing=True, eager_replay=True, staging=args.staging, replay_mode=args.replay_mode)
+                   timing=True, eager_replay=True, staging=args.staging, replay_mode=args.replay_mode,
+                   stream_buffers=args.stream_buffers)
     baseline = args.scheme != "gockpt"
     if baseline:
         snap_host = [torch.empty(n, dtype=torch.float32, pin_memory=True) for _ in range(3)]
@@ -507,7 +510,8 @@ def main():
                   "note": "gck_recommend_k(n, measured link GB/s, checkpoint-free step time)"},
         "replay": {"host_ms_last_session": st1["last_replay_ms"], "threads": st1["replay_threads"],
                    "worker_ms_last_session": st1["last_worker_ms"],
-                   "finalize_wait_ms_last": st1["last_finalize_wait_ms"],
+                   "finalize_wait_ms_last": st1["last_finalize_wait_ms"], "mode": args.replay_mode,
+                   "stream_wait_ms_last": st1.get("last_stream_wait_ms"),
                    "timing_note": "host_ms = the replay arithmetic; worker/finalize_wait are host wall times "
                                   "from the moment the host enqueued step K (the host runs up to an interval "
                                   "ahead of the GPU), so they include waiting for the queued steps to execute",

@@ -74,7 +74,7 @@ typedef struct {
 } gck_hparams;
 
 enum { GCK_COPY_ENGINE = 0, GCK_COPY_ZEROCOPY = 1 };
-enum { GCK_REPLAY_HOST = 0, GCK_REPLAY_GPU = 1, GCK_REPLAY_DEFERRED = 2 };
+enum { GCK_REPLAY_HOST = 0, GCK_REPLAY_GPU = 1, GCK_REPLAY_DEFERRED = 2, GCK_REPLAY_STREAM = 3 };
 enum { GCK_STAGE_RING = 0, GCK_STAGE_DIRECT = 1, GCK_STAGE_BLOCKING = 2 };
 
 typedef struct {
@@ -98,7 +98,15 @@ typedef struct {
                                does no replay — the handle holds the captured parts (replay_pending = 1),
                                gck_persist_begin writes them with the gradient log and StepRecords
                                (file version 2), and the replay runs at load time: on the GPU inside
-                               gck_restore, on the host inside gck_load_checkpoint(_range) */
+                               gck_restore, on the host inside gck_load_checkpoint(_range);
+                               GCK_REPLAY_STREAM (streaming host replay):
+                               a library thread started at begin applies update t0+i to the prefix
+                               [0, hi_i) as soon as slice i has drained (parts 1..i are then all at
+                               S(t0+i)), so the gradient log is a ring of stream_buffers slices of n
+                               elements (pinned arena 12n + 2n*B bytes instead of 12n + n(K-1));
+                               gck_submit blocks (host) before reusing a slice buffer whose update has
+                               not been applied yet. Same per-element op order as the batch replay.
+                               Always eager; gck_get_staged / gck_replay_gpu are PROTOCOL errors */
     int32_t replay_threads; /* host replay threads (0 -> all cores of the affinity mask) */
     int32_t timing;         /* 1: record CUDA events for stall / kernel / D2H times (gck_stats) */
     int32_t eager_replay;   /* 1: replay starts on a library thread as soon as the gradient log is
@@ -117,6 +125,8 @@ typedef struct {
                                >= 0 binds them to that NUMA node; -1 = the GPU's own node (from its PCI
                                address; no binding if the platform reports none); -2 = no binding.
                                P:401: "28 cores per process, same NUMA domain". */
+    uint32_t stream_buffers; /* GCK_REPLAY_STREAM: gradient slice buffers B (0 -> 2); ignored otherwise */
+    uint32_t _pad_cfg;
 } gck_config;
 
 /* Caller-owned device tensors (PyTorch owns them; they must outlive the context). */
@@ -191,6 +201,7 @@ typedef struct {
     uint32_t _pad2;
     double auto_step_ms;           /* step time the last automatic K used (0: not measured) */
     double auto_link_gbs;          /* link rate the last automatic K used */
+    double last_stream_wait_ms;    /* GCK_REPLAY_STREAM: host time gck_submit blocked on slice-buffer reuse */
 } gck_stats;
 
 /* ---- context lifecycle -------------------------------------------------- */

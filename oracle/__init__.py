@@ -15,7 +15,8 @@ Modules
                 (O1: plain synchronous trajectory S(0) -> S(T)).
   partition.py  a1 partition plan (parts, gradient prefixes, byte counts).
   replay.py     O2: the plain K-step partitioned capture + gradient-assisted
-                replay, exactly in the paper's order.
+                replay, exactly in the paper's order; plus its
+                streaming form (updates applied as the slices arrive).
 
 Numerics: every floating-point operation is an IEEE binary32 numpy operation
 (round-to-nearest-even, no FMA contraction, denormals kept), in the operation
@@ -32,10 +33,10 @@ SPEC's make_parts examples and closed-form byte counts. No function here is
 
 from .adamw import StepRecord, make_step_record, adamw_update, rne_bf16, bf16_to_f32, trajectory
 from .partition import make_parts, grad_prefix, session_bytes, slot_bytes
-from .replay import capture_session, replay, assemble, oracle_session
+from .replay import capture_session, replay, replay_streaming, assemble, oracle_session
 
 __all__ = [
     "StepRecord", "make_step_record", "adamw_update", "rne_bf16", "bf16_to_f32", "trajectory",
     "make_parts", "grad_prefix", "session_bytes", "slot_bytes",
-    "capture_session", "replay", "assemble", "oracle_session",
+    "capture_session", "replay", "replay_streaming", "assemble", "oracle_session",
 ]

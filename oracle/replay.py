@@ -74,6 +74,21 @@ def replay(cap, glog, recs, parts):
     return p, m, v
 
 
+def replay_streaming(cap, glog, recs, parts):
+    """Streaming form of the same replay (SURVEY §8(a) a5 "Streaming"; P:345's updates applied as
+    the slices arrive): the parts land in order; once part i and G(t0+i)[0:hi_i] are on the host
+    (i < K), update t0+i is applied to the whole prefix [0, hi_i) = parts 1..i, which are then all
+    at S(t0+i). Element e of part j receives updates t0+j .. t0+K-1 in ascending order, the batch
+    order, so the result must equal replay() bit for bit.
+    """
+    K = len(parts)
+    p, m, v = assemble(cap)                     # part i's bytes are only read after it "lands"
+    for i in range(1, K):
+        hi = parts[i - 1][1]
+        p[:hi], m[:hi], v[:hi], _ = adamw_update(p[:hi], m[:hi], v[:hi], glog[i - 1][:hi], recs[i - 1])
+    return p, m, v
+
+
 def oracle_session(p0, m0, v0, grads, recs, K: int, A: int = 1):
     """Full O2 on [0, n): plan, capture over K steps, replay. Returns (ckpt, cap, glog, parts, live)."""
     n = len(p0)

@@ -25,7 +25,7 @@ K_LIMIT = 64
 STATUS_NAMES = ["GCK_OK", "GCK_E_INVALID", "GCK_E_PROTOCOL", "GCK_E_STALE", "GCK_E_NOMEM", "GCK_E_CUDA",
                 "GCK_E_INCOMPLETE", "GCK_E_ABORTED", "GCK_E_BUSY", "GCK_E_NODEVICE", "GCK_E_IO", "GCK_E_CORRUPT"]
 COPY_ENGINE, COPY_ZEROCOPY = 0, 1
-REPLAY_HOST, REPLAY_GPU, REPLAY_DEFERRED = 0, 1, 2
+REPLAY_HOST, REPLAY_GPU, REPLAY_DEFERRED, REPLAY_STREAM = 0, 1, 2, 3
 STAGE_RING, STAGE_DIRECT, STAGE_BLOCKING = 0, 1, 2
 
 
@@ -39,7 +39,7 @@ class Config(C.Structure):
                 ("ring_slots", C.c_uint32), ("copy_mode", C.c_int32), ("chunk_bytes", C.c_uint64),
                 ("zc_ctas", C.c_uint32), ("replay_mode", C.c_int32), ("replay_threads", C.c_int32),
                 ("timing", C.c_int32), ("eager_replay", C.c_int32), ("staging", C.c_int32),
-                ("numa_node", C.c_int32)]
+                ("numa_node", C.c_int32), ("stream_buffers", C.c_uint32), ("_pad_cfg", C.c_uint32)]
 
 
 class Tensors(C.Structure):
@@ -80,7 +80,7 @@ class Stats(C.Structure):
                 ("last_finalize_wait_ms", C.c_double), ("last_session_d2h_bytes", C.c_uint64),
                 ("gpu_launches", C.c_uint64), ("replay_threads", C.c_int32), ("numa_node", C.c_int32),
                 ("last_session_k", C.c_uint32), ("_pad2", C.c_uint32), ("auto_step_ms", C.c_double),
-                ("auto_link_gbs", C.c_double)]
+                ("auto_link_gbs", C.c_double), ("last_stream_wait_ms", C.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_ if not k.startswith("_")}

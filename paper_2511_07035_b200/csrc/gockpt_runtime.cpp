@@ -248,6 +248,14 @@ struct gck_ctx {
     double replay_compute_ms = 0;  // the host replay itself
     int replay_threads_used = 0;
 
+    // streaming replay (GCK_REPLAY_STREAM): slices land in B recycled buffers of slice_elems
+    bool stream_mode = false;
+    uint32_t B = 2;
+    uint64_t slice_elems = 0;
+    uint32_t submitted = 0;        // session steps whose drain (and done event) is enqueued
+    uint32_t applied = 0;          // slices whose update the stream worker has applied
+    bool stream_cancel = false;    // abort / destroy: the worker stops waiting for submits
+
     // GPU replay mode: library-owned device scratch + stream for the staged-parts round trip
     cudaStream_t rstream = nullptr;
     char *rscratch = nullptr;
@@ -286,6 +294,80 @@ struct gck_ctx {
     void abort_session(cudaError_t e, const char *what) {
         state = State::ABORTED;
         last_error = std::string("checkpoint aborted: ") + what + ": " + cudaGetErrorString(e);
+        cancel_stream();
+    }
+    void cancel_stream() {
+        std::lock_guard<std::mutex> lk(mu);
+        stream_cancel = true;
+        cv.notify_all();
+    }
+
+    // a5, streaming (GCK_REPLAY_STREAM): as soon as session step i+1 has drained (part i+1 at
+    // S(t0+i), slice i = G(t0+i+1)[0:hi_i]), apply update t0+i+1 to the prefix [0, hi_i): parts
+    // 1..i+1 are then all at S(t0+i+1). After slice K-2, parts 1..K-1 are at S(T). Each element of
+    // part j gets updates t0+j .. T in ascending order — the batch replay's op sequence.
+    void run_stream() {
+        const auto t_start = std::chrono::steady_clock::now();
+        gck_status st = GCK_OK;
+        double comp = 0;
+        {
+            DeviceGuard g(cfg.device);
+            for (uint32_t i = 0; i + 1 < K && st == GCK_OK; ++i) {
+                {
+                    std::unique_lock<std::mutex> lk(mu);
+                    cv.wait(lk, [&] { return stream_cancel || submitted > i; });
+                    if (stream_cancel) {
+                        st = GCK_E_ABORTED;
+                        break;
+                    }
+                }
+                if (cudaEventSynchronize(done[i]) != cudaSuccess) {
+                    st = GCK_E_ABORTED;
+                    break;
+                }
+                const auto r0 = std::chrono::steady_clock::now();
+                const gck_step_record r2[2] = {recs[i], recs[i]};
+                const uint64_t lo2[2] = {0, hi[i]}, hi2[2] = {hi[i], cfg.n};
+                const uint16_t *g2[2] = {glog[i], nullptr};
+                st = gck::replay_host_impl(r2, 2, lo2, hi2, h_master, h_m, h_v, g2, cfg.replay_threads,
+                                           &replay_threads_used, numa >= 0 ? &numa_cpus : nullptr);
+                comp += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - r0).count();
+                std::lock_guard<std::mutex> lk(mu);
+                applied = i + 1;
+                cv.notify_all();
+            }
+            if (st == GCK_OK) {  // the last part (no gradient) landed
+                std::unique_lock<std::mutex> lk(mu);
+                cv.wait(lk, [&] { return stream_cancel || submitted >= K; });
+                if (stream_cancel) st = GCK_E_ABORTED;
+                lk.unlock();
+                if (st == GCK_OK && cudaEventSynchronize(done[K - 1]) != cudaSuccess) st = GCK_E_ABORTED;
+            }
+        }
+        const double ms =
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+        std::lock_guard<std::mutex> lk(mu);
+        replay_compute_ms = comp;
+        replay_ms = ms;
+        replayed = (st == GCK_OK);
+        worker_status = st;
+        worker_done = true;
+        applied = K;  // never leave a submit waiting on a dead worker
+        cv.notify_all();
+    }
+
+    // Streaming: before the drain of session step i writes slice buffer (i-1) mod B, the update
+    // of the slice that used it last (i-B) must have been applied. Host wait; timed.
+    gck_status stream_slot_wait(uint32_t i) {
+        if (!stream_mode || i >= K || i <= B) return GCK_OK;
+        const auto w0 = std::chrono::steady_clock::now();
+        std::unique_lock<std::mutex> lk(mu);
+        cv.wait(lk, [&] { return applied >= i - B || worker_done; });
+        const bool ok = applied >= i - B && !(worker_done && worker_status != GCK_OK);
+        lk.unlock();
+        stats.last_stream_wait_ms +=
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count();
+        return ok ? GCK_OK : GCK_E_ABORTED;
     }
 
     void record_for(uint64_t adam_t, double lr, double gs, int32_t skip, gck_step_record *out) {
@@ -598,7 +680,7 @@ gck_status gck_create(const gck_config *cfg_in, const gck_hparams *hp, const gck
     if (cfg.copy_mode != GCK_COPY_ENGINE && cfg.copy_mode != GCK_COPY_ZEROCOPY)
         return set_tls(GCK_E_INVALID, "bad copy_mode");
     if (cfg.replay_mode != GCK_REPLAY_HOST && cfg.replay_mode != GCK_REPLAY_GPU &&
-        cfg.replay_mode != GCK_REPLAY_DEFERRED)
+        cfg.replay_mode != GCK_REPLAY_DEFERRED && cfg.replay_mode != GCK_REPLAY_STREAM)
         return set_tls(GCK_E_INVALID, "bad replay_mode");
     if (!(hp->beta1 > 0 && hp->beta1 < 1 && hp->beta2 > 0 && hp->beta2 < 1 && hp->eps > 0 && hp->weight_decay >= 0))
         return set_tls(GCK_E_INVALID, "hyperparameters out of range");
@@ -629,6 +711,16 @@ gck_status gck_create(const gck_config *cfg_in, const gck_hparams *hp, const gck
     c->direct = (cfg.staging == GCK_STAGE_DIRECT || cfg.staging == GCK_STAGE_BLOCKING);
     c->blocking_grad = (cfg.staging == GCK_STAGE_BLOCKING);
     c->slot_bytes = c->direct ? 0 : slot_max;
+    c->stream_mode = (cfg.replay_mode == GCK_REPLAY_STREAM);
+    if (c->stream_mode) {  // a ring of B slice buffers replaces the full gradient log
+        if (cfg.stream_buffers > GCK_K_LIMIT) {
+            delete c;
+            return set_tls(GCK_E_INVALID, "stream_buffers must be <= 64");
+        }
+        c->B = cfg.stream_buffers ? cfg.stream_buffers : 2;
+        c->slice_elems = align_up(cfg.n, 128);
+        glog_max = (uint64_t)c->B * c->slice_elems;
+    }
     c->glog_elems_cap = glog_max;
     cudaError_t e = cudaSuccess;
     if (!c->direct && t->ring) {  // caller-owned ring (e.g. from the PyTorch caching allocator)
@@ -708,6 +800,7 @@ gck_status gck_create(const gck_config *cfg_in, const gck_hparams *hp, const gck
 
 gck_status gck_destroy(gck_ctx *c) {
     if (!c) return GCK_OK;
+    c->cancel_stream();
     c->join_worker();
     c->join_persist();
     {
@@ -806,6 +899,7 @@ gck_status gck_begin_checkpoint(gck_ctx *c, uint64_t t0, uint32_t K) {
     if (K < c->cfg.k_min || K > c->cfg.k_max) return c->fail(GCK_E_INVALID, "K outside [k_min, k_max]");
     c->stats.last_session_k = K;
     if (c->state == State::ABORTED) {  // drain whatever the aborted session left queued
+        c->cancel_stream();
         c->join_worker();
         DeviceGuard g(c->cfg.device);
         cudaStreamSynchronize(c->d2h);
@@ -816,6 +910,10 @@ gck_status gck_begin_checkpoint(gck_ctx *c, uint64_t t0, uint32_t K) {
     uint64_t off = 0;
     for (uint32_t i = 0; i < K; ++i) {
         const uint64_t ghi = (i + 1 < K) ? c->hi[i] : 0;
+        if (c->stream_mode) {  // B recycled slice buffers
+            c->glog[i] = ghi ? c->h_glog + (uint64_t)(i % c->B) * c->slice_elems : nullptr;
+            continue;
+        }
         c->glog[i] = ghi ? c->h_glog + off : nullptr;
         off += align_up(ghi, 128);
     }
@@ -837,6 +935,14 @@ gck_status gck_begin_checkpoint(gck_ctx *c, uint64_t t0, uint32_t K) {
     c->replay_ms = 0;
     c->replay_compute_ms = 0;
     c->state = State::ACTIVE;
+    if (c->stream_mode) {  // the streaming worker follows the drains from the first one on
+        c->join_worker();
+        c->submitted = c->applied = 0;
+        c->stream_cancel = false;
+        c->stats.last_stream_wait_ms = 0;
+        c->worker_started = true;
+        c->worker = std::thread([c]() { c->run_stream(); });
+    }
     return GCK_OK;
 }
 
@@ -898,10 +1004,15 @@ static gck_status enqueue_drain(gck_ctx *c, uint32_t i, const SlotLayout &L, cha
 
 static void finish_session_step(gck_ctx *c, uint32_t i) {
     c->next_part++;
+    if (c->stream_mode) {
+        std::lock_guard<std::mutex> lk(c->mu);
+        c->submitted = i;
+        c->cv.notify_all();
+    }
     if (i == c->K) {
         c->state = State::DRAINING;
         c->stats.sessions++;
-        if (c->cfg.eager_replay) {
+        if (c->cfg.eager_replay && !c->stream_mode) {
             c->worker_started = true;
             c->worker = std::thread([c]() { c->run_replay(); });
         }
@@ -918,6 +1029,10 @@ static gck_status submit_direct(gck_ctx *c, uint32_t i, const gck_step_args *a, 
     cudaError_t e;
     if (i < c->K) {
         const uint64_t ghi = c->hi[i - 1];
+        if (c->stream_slot_wait(i) != GCK_OK) {
+            c->abort_session(cudaSuccess, "streaming replay failed");
+            return GCK_E_ABORTED;
+        }
         if ((e = cudaEventRecord(c->ev_grad_src, s)) != cudaSuccess ||
             (e = cudaStreamWaitEvent(c->d2h, c->ev_grad_src, 0)) != cudaSuccess) {
             c->abort_session(e, "direct: gradient event");
@@ -1076,6 +1191,10 @@ gck_status gck_submit(gck_ctx *c, uint32_t part, const gck_step_args *a, void *s
         c->abort_session(e, "pack event");
         return GCK_E_ABORTED;
     }
+    if (c->stream_slot_wait(i) != GCK_OK) {
+        c->abort_session(cudaSuccess, "streaming replay failed");
+        return GCK_E_ABORTED;
+    }
     if (c->cfg.timing) cudaEventRecord(c->ev_d0[i - 1], c->d2h);
     if (enqueue_drain(c, i, L, slot) != GCK_OK) {
         c->abort_session(cudaGetLastError(), "drain enqueue");
@@ -1105,7 +1224,7 @@ gck_status gck_wait_drained(gck_ctx *c) {
 
 gck_status gck_get_staged(gck_ctx *c, gck_staged *out) {
     if (!c || !out) return set_tls(GCK_E_INVALID, "null argument");
-    if (c->state != State::DRAINING || c->worker_started || c->replayed)
+    if (c->state != State::DRAINING || c->worker_started || c->replayed || c->stream_mode)
         return c->fail(GCK_E_PROTOCOL, "staged bytes are only visible between part K and finalize with eager_replay=0");
     if (cudaEventQuery(c->done[c->K - 1]) != cudaSuccess) return c->fail(GCK_E_PROTOCOL, "call gck_wait_drained first");
     std::memset(out, 0, sizeof(*out));
@@ -1195,7 +1314,7 @@ gck_status gck_sync_snapshot(gck_ctx *c, void *stream, float *h_master, float *h
 
 gck_status gck_replay_gpu(gck_ctx *c, void *stream, float *d_master, float *d_m, float *d_v, uint16_t *d_glog) {
     if (!c || !d_master || !d_m || !d_v || !d_glog) return set_tls(GCK_E_INVALID, "null argument");
-    if (c->state != State::DRAINING || c->worker_started || c->replayed)
+    if (c->state != State::DRAINING || c->worker_started || c->replayed || c->stream_mode)
         return c->fail(GCK_E_PROTOCOL, "gck_replay_gpu needs the staged bytes (eager_replay=0, before finalize)");
     if (!aligned16(d_master) || !aligned16(d_m) || !aligned16(d_v) || !aligned16(d_glog))
         return c->fail(GCK_E_INVALID, "device arrays must be 16-byte aligned");

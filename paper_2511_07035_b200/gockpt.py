@@ -230,7 +230,7 @@ class GoCkpt:
     def __init__(self, master, exp_avg, exp_avg_sq, param_bf16=None, *, beta1=0.9, beta2=0.999, eps=1e-8,
                  weight_decay=0.01, k_min=1, k_max=8, part_align=1024, ring_slots=2, copy_mode="ce",
                  chunk_bytes=0, zc_ctas=0, replay_threads=0, timing=True, eager_replay=True, staging="ring",
-                 numa_node=-1, replay_mode="host", ring=None):
+                 numa_node=-1, replay_mode="host", ring=None, stream_buffers=0):
         n = master.numel()
         if exp_avg.numel() != n or exp_avg_sq.numel() != n or (param_bf16 is not None and param_bf16.numel() != n):
             raise ValueError("state tensors must have the same number of elements")
@@ -238,11 +238,12 @@ class GoCkpt:
         self._keep = (master, exp_avg, exp_avg_sq, param_bf16)
         cfg = L.Config(L.ABI_VERSION, master.device.index or 0, n, k_min, k_max, part_align, ring_slots,
                        {"ce": L.COPY_ENGINE, "zerocopy": L.COPY_ZEROCOPY}[copy_mode], chunk_bytes, zc_ctas,
-                       {"host": L.REPLAY_HOST, "gpu": L.REPLAY_GPU, "deferred": L.REPLAY_DEFERRED}[replay_mode],
+                       {"host": L.REPLAY_HOST, "gpu": L.REPLAY_GPU, "deferred": L.REPLAY_DEFERRED,
+                        "stream": L.REPLAY_STREAM}[replay_mode],
                        replay_threads, int(timing),
                        int(eager_replay),
                        {"ring": L.STAGE_RING, "direct": L.STAGE_DIRECT, "blocking": L.STAGE_BLOCKING}[staging],
-                       numa_node)
+                       numa_node, stream_buffers)
         hp = L.Hparams(beta1, beta2, eps, weight_decay)
         self.hparams = dict(beta1=beta1, beta2=beta2, eps=eps, weight_decay=weight_decay)
         # ring: an optional caller-owned uint8 CUDA tensor of >= ring_bytes_required(...) bytes

@@ -28,6 +28,9 @@ class CheckpointedAdamW:
     def __init__(self, master, exp_avg, exp_avg_sq, param_bf16=None, *, lr=1e-3, betas=(0.9, 0.999), eps=1e-8,
                  weight_decay=0.01, K=8, k_min=None, k_max=None, step=0, adam_t=None, persist_dir=None,
                  rank=0, world=1, on_checkpoint=None, **ctx_kw):
+        if ctx_kw.get("replay_mode") == "deferred" and not persist_dir:
+            raise ValueError("replay_mode='deferred' materialises S(T) only when the file is loaded: "
+                             "it needs persist_dir")
         self.K = K
         self.lr = lr
         self.ctx = GoCkpt(master, exp_avg, exp_avg_sq, param_bf16, beta1=betas[0], beta2=betas[1], eps=eps,
@@ -111,6 +114,20 @@ class CheckpointedAdamW:
             raise RuntimeError("a session is still collecting parts: run K more steps first")
         self._settle(block=True)
         return self.last
+
+    def restore(self, path: str | None = None, stream=None) -> dict:
+        """Load a persisted checkpoint (the LATEST of this rank if path is None) into the device
+        state and resume after it: version-1 files upload S(T); version-2 (replay-on-restore)
+        files are replayed on the GPU in place. Returns the file header."""
+        if self._session is not None or self._draining is not None or self._held:
+            raise RuntimeError("restore while a checkpoint session is live")
+        if path is None:
+            latest = os.path.join(self.persist_dir or ".", f"LATEST.rank{self.rank}")
+            with open(latest) as fh:
+                path = os.path.join(os.path.dirname(latest), fh.read().strip())
+        h = self.ctx.restore(path, stream)
+        self.global_step, self.adam_t = h["step"], h["adam_t"]
+        return h
 
     def close(self):
         try:

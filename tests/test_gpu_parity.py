@@ -389,6 +389,69 @@ def test_deferred_replay_session_restore(G, tmp_path, n, K, A, staging):
     ctx.close()
 
 
+# ---------------------------------------------------------------- a5 streaming host replay
+@pytest.mark.parametrize("n,K,A,B,staging,copy", [(1 << 20, 4, 1024, 2, "ring", "ce"),
+                                                  (1_000_003, 8, 1024, 2, "ring", "ce"),
+                                                  (1_000_003, 8, 1024, 1, "ring", "zerocopy"),
+                                                  (300_007, 6, 8, 3, "direct", "ce"),
+                                                  (5000, 2, 8, 2, "ring", "ce"),
+                                                  ((1 << 18) + 4101, 16, 1024, 4, "ring", "ce"),
+                                                  (1 << 20, 1, 1024, 2, "ring", "ce")])
+def test_streaming_replay_session(G, n, K, A, B, staging, copy):
+    """replay_mode="stream": slice i's update is applied to [0, hi_i) as soon as it drains, the
+    gradient log is a ring of B buffers (the next drain into a buffer waits for its update).
+    Result == the oracle's S(T) and == the GPU's own sync snapshot, bit for bit, with a skipped
+    update inside the session."""
+    t0, seed = 10, 19
+    state, grads, recs, sargs = session_inputs(seed, n, K, t0, skips=(t0 + 2,) if K >= 3 else ())
+    ctx, (p, m, v, out) = _make_ctx(G, state, K, part_align=A, staging=staging, copy_mode=copy,
+                                    replay_mode="stream", stream_buffers=B)
+    want = oracle.trajectory(*state, grads[:K - 1], recs[:K - 1])[-1]
+    ctx.begin_checkpoint(t0, K)
+    gbuf = None
+    for i in range(1, K + 1):
+        a = sargs[i - 1]
+        if i == K:
+            snap = ctx.sync_snapshot()
+        if staging == "direct":
+            if gbuf is None:
+                gbuf = up_u16(grads[i - 1])
+            else:
+                gbuf.copy_(up_u16(grads[i - 1]))
+            ctx.submit(i, a["step"], a["adam_t"], a["lr"], gbuf, a["grad_scale"], a["skip"])
+            ctx.grad_fence()
+        else:
+            ctx.submit(i, a["step"], a["adam_t"], a["lr"], up_u16(grads[i - 1]), a["grad_scale"], a["skip"])
+    ck = ctx.finalize()
+    assert ck.step == t0 + K - 1 and not ck.replay_pending
+    assert_state_equal((ck.master, ck.exp_avg, ck.exp_avg_sq), snap, "stream vs GPU sync snapshot")
+    assert_state_equal((ck.master, ck.exp_avg, ck.exp_avg_sq), want, "stream vs oracle")
+    st = ctx.stats()
+    assert st["last_stream_wait_ms"] >= 0 and st["last_session_k"] == K
+    ctx.release()
+    # a second session on the same context (buffers reused across sessions)
+    t1 = t0 + K
+    state2 = (down_f32(p), down_f32(m), down_f32(v))
+    g2 = [gi.grad_bits(seed + 1, t1 + i, n) for i in range(1, K + 1)]
+    ctx.begin_checkpoint(t1, K)
+    for i in range(1, K + 1):
+        gg = up_u16(g2[i - 1])
+        if staging == "direct":
+            gbuf.copy_(gg)
+            gg = gbuf
+        ctx.submit(i, t1 + i, sargs[-1]["adam_t"] + i, 1e-3, gg)
+        if staging == "direct":
+            ctx.grad_fence()
+    ck = ctx.finalize()
+    recs2 = [oracle.make_step_record(t=sargs[-1]["adam_t"] + i, lr=1e-3, **HP) for i in range(1, K + 1)]
+    assert_state_equal((ck.master, ck.exp_avg, ck.exp_avg_sq),
+                       oracle.trajectory(*state2, g2[:K - 1], recs2[:K - 1])[-1], "second session")
+    with pytest.raises(Exception):
+        ctx.staged()                                   # no staged view in streaming mode
+    ctx.release()
+    ctx.close()
+
+
 # ---------------------------------------------------------------- NEXT-2: direct staging (GoCkpt-O literal)
 @pytest.mark.parametrize("n,K,A,copy,staging", [(1 << 20, 4, 1024, "ce", "direct"), (1_000_003, 8, 1024, "ce", "direct"),
                                                 (300_007, 3, 8, "zerocopy", "direct"), (1 << 20, 1, 1024, "ce", "direct"),
@@ -455,8 +518,9 @@ def test_c_api_demo_program(G, tmp_path, repo_root):
 
 
 # ---------------------------------------------------------------- failure path: checkpoint aborted, training continues
-@pytest.mark.parametrize("staging", ["ring", "direct"])
-def test_drain_failure_aborts_checkpoint_not_training(G, staging):
+@pytest.mark.parametrize("staging,replay_mode", [("ring", "host"), ("direct", "host"), ("ring", "stream"),
+                                                 ("direct", "stream")])
+def test_drain_failure_aborts_checkpoint_not_training(G, staging, replay_mode):
     """a transfer-channel failure aborts the checkpoint (finalize reports it)
     while every optimizer update still runs; the next session works normally."""
     from paper_2511_07035_b200 import GckError
@@ -464,7 +528,8 @@ def test_drain_failure_aborts_checkpoint_not_training(G, staging):
     n, K, t0, seed = 300_007, 4, 10, 13
     state, grads, recs, sargs = session_inputs(seed, n, 2 * K, t0)
     p, m, v = (up_f32(x) for x in state)
-    ctx = G.GoCkpt(p, m, v, None, **HP, k_min=K, k_max=K, part_align=64, staging=staging)
+    ctx = G.GoCkpt(p, m, v, None, **HP, k_min=K, k_max=K, part_align=64, staging=staging, replay_mode=replay_mode,
+                   stream_buffers=1)
     os.environ["GCK_FAULT_DRAIN"] = "2"
     try:
         ctx.begin_checkpoint(t0, K)
@@ -659,9 +724,12 @@ def test_automatic_k(G):
     ctx.close()
 
 
-def test_checkpointed_adamw_training_loop(G, tmp_path):
+@pytest.mark.parametrize("replay_mode", ["host", "deferred"])
+def test_checkpointed_adamw_training_loop(G, tmp_path, replay_mode):
     """The optimizer face (save_checkpoint / step / wait): checkpoints requested every 12 steps
-    while training runs, each consistent == the oracle's state at its step and durable on disk."""
+    while training runs, each consistent == the oracle's state at its step and durable on disk.
+    deferred (replay-on-restore): the handles hold the captured parts, the files S(T) after the
+    oracle's replay, and opt.restore() brings the device state back to S(39) through the GPU replay."""
     from paper_2511_07035_b200.optim import CheckpointedAdamW
     from oracle import ckpt_file as OF
     n, K, seed, steps = 300_007, 4, 51, 40
@@ -669,6 +737,7 @@ def test_checkpointed_adamw_training_loop(G, tmp_path):
     p, m, v = (up_f32(x) for x in state)
     got = {}
     opt = CheckpointedAdamW(p, m, v, None, lr=1e-3, K=K, part_align=64, persist_dir=str(tmp_path),
+                            replay_mode=replay_mode,
                             on_checkpoint=lambda ck: got.__setitem__(ck.step, (ck.master.copy(), ck.exp_avg.copy(),
                                                                                ck.exp_avg_sq.copy())))
     ref, traj = tuple(x.copy() for x in state), {0: tuple(x.copy() for x in state)}
@@ -683,14 +752,19 @@ def test_checkpointed_adamw_training_loop(G, tmp_path):
         ref = oracle.adamw_update(*ref, g, oracle.make_step_record(t=s, lr=1e-3, **HP))[:3]
         traj[s] = tuple(x.copy() for x in ref)
     last = opt.wait()
-    opt.close()
     assert sorted(got) == [K - 1 + 12 * k for k in range(4)] == [3, 15, 27, 39]
-    for step, st in got.items():
-        assert_state_equal(st, traj[step], f"checkpoint at {step}")
+    if replay_mode == "host":
+        for step, st in got.items():
+            assert_state_equal(st, traj[step], f"checkpoint at {step}")
     assert last[0] == 39 and OF.latest(str(tmp_path)) == last[1]
-    hdr, fp, fm, fv = OF.read(last[1])
+    hdr, fp, fm, fv = OF.read_consistent(last[1])
     assert hdr["step"] == 39 and hdr["adam_t"] == 39
     assert_state_equal((fp, fm, fv), traj[39], "persisted")
+    h = opt.restore()                                        # device state back to S(39)
+    torch.cuda.synchronize()
+    assert h["step"] == 39 and opt.global_step == 39 and opt.adam_t == 39
+    assert_state_equal((down_f32(p), down_f32(m), down_f32(v)), traj[39], "restored")
+    opt.close()
 
 
 # ---------------------------------------------------------------- T2 on one GPU: R shards, R contexts

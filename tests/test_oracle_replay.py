@@ -13,7 +13,7 @@ import numpy as np
 import pytest
 
 from oracle import (adamw_update, make_step_record, trajectory, make_parts, grad_prefix,
-                    session_bytes, slot_bytes, capture_session, replay, oracle_session)
+                    session_bytes, slot_bytes, capture_session, replay, replay_streaming, oracle_session)
 import gockpt_inputs as gi
 
 HP = dict(beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01)
@@ -125,6 +125,8 @@ def test_brute_force_every_partition(mode, t0):
                 for parts in compositions(n, K):
                     cap, glog, _ = capture_session(p0, m0, v0, grads, recs, parts)
                     assert states_equal(replay(cap, glog, recs, parts), target), (seed, n, K, parts)
+                    # the streaming order (slices applied as they land) reaches the same bytes
+                    assert states_equal(replay_streaming(cap, glog, recs, parts), target), (seed, n, K, parts)
                     count += 1
     assert count == 5 * (2 ** 9 - 1)
 
