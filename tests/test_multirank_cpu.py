@@ -28,7 +28,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, n_total, K, t0, result_dir):
+def _worker(rank, world, port, n_total, K, t0, result_dir, deferred=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
@@ -52,12 +52,18 @@ def _worker(rank, world, port, n_total, K, t0, result_dir):
         cap, glog, _ = oracle.capture_session(p0, m0, v0, grads, recs, parts)
         p, m, v = (np.ascontiguousarray(x) for x in oracle.assemble(cap))
         lrecs = [G.make_step_record(0.9, 0.999, 1e-8, 0.01, t0 + i, 1e-3) for i in range(1, K + 1)]
+        cp, cm, cv = p.copy(), m.copy(), v.copy()           # the captured parts (replay-on-restore file)
         G.replay_host(lrecs, parts, p, m, v, [np.ascontiguousarray(x) for x in glog], threads=2)
         np.save(os.path.join(result_dir, f"rank{rank}.npy"), np.stack([p, m, v]))
         # NEXT-1 per-rank persistence + rank-0 global commit
         from paper_2511_07035_b200.harness import commit_global
         path = os.path.join(result_dir, f"ckpt_{t0 + K - 1}.rank{rank}.bin")
-        G.write_checkpoint(path, p, m, v, step=t0 + K - 1, adam_t=t0 + K - 1, rank=rank, world=world, threads=2)
+        if deferred:      # version 2: captured parts + gradient log; every loader replays
+            G.write_checkpoint_log(path, cp, cm, cv, t0=t0, parts=parts, recs=lrecs,
+                                   glog=[np.ascontiguousarray(x) for x in glog], adam_t=t0 + K - 1, rank=rank,
+                                   world=world, threads=2)
+        else:
+            G.write_checkpoint(path, p, m, v, step=t0 + K - 1, adam_t=t0 + K - 1, rank=rank, world=world, threads=2)
         assert commit_global(result_dir, t0 + K - 1, True, n_total=n_total, n_per_rank=n_r, align=64)
         t = max_over_ranks(float(rank + 1))
         assert t == float(world)
@@ -68,10 +74,10 @@ def _worker(rank, world, port, n_total, K, t0, result_dir):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n_total", [10_000, 4096 * 3 + 17])
-def test_two_ranks_shard_checkpoints_concatenate_to_global(tmp_path, n_total):
+@pytest.mark.parametrize("n_total,deferred", [(10_000, False), (4096 * 3 + 17, False), (4096 * 3 + 17, True)])
+def test_two_ranks_shard_checkpoints_concatenate_to_global(tmp_path, n_total, deferred):
     world, K, t0 = 2, 4, 20
-    mp.spawn(_worker, args=(world, _free_port(), n_total, K, t0, str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), n_total, K, t0, str(tmp_path), deferred), nprocs=world, join=True)
     from paper_2511_07035_b200.harness import zero1_shard
     _, n_r, padded = zero1_shard(n_total, world, 0, align=64)
     got = np.concatenate([np.load(tmp_path / f"rank{r}.npy") for r in range(world)], axis=1)
@@ -87,7 +93,7 @@ def test_two_ranks_shard_checkpoints_concatenate_to_global(tmp_path, n_total):
     from oracle import ckpt_file as OF
     man = json.load(open(tmp_path / "MANIFEST.json"))
     assert man["step"] == t0 + K - 1 and man["world"] == world
-    back = np.concatenate([np.stack(OF.read(str(tmp_path / f))[1:]) for f in man["files"]], axis=1)
+    back = np.concatenate([np.stack(OF.read_consistent(str(tmp_path / f))[1:]) for f in man["files"]], axis=1)
     assert np.array_equal(back.view(np.uint32), got.view(np.uint32))
     # load into other data-parallel degrees (resharding): the concatenation over the new ranks is S(T)
     from paper_2511_07035_b200.harness import load_resharded
