@@ -454,6 +454,11 @@ def main():
                          f"{dt:.1f} s measured, time scaled x{n / n_s:.1f}; AdamW + capture + replay only, no F/B"}
 
     sess_stall_delta = [max(0.0, t - free_med) for t in sess_ms]
+    # bootstrap 95% CI of the mean delta per session step, resampling whole sessions
+    per_sess = [statistics.mean(sess_stall_delta[k:k + K_aff]) for k in range(0, len(sess_stall_delta), K_aff)]
+    rng = np.random.default_rng(0)
+    boot = [float(np.mean(rng.choice(per_sess, len(per_sess)))) for _ in range(2000)]
+    delta_ci95 = [float(np.percentile(boot, 2.5)), float(np.percentile(boot, 97.5))]
     ctx_stats_final = ctx.stats()
     # NEXT-4: the analytic model's K for this step time and link (smallest K whose largest per-step
     # transfer fits in one step), next to the K this run used
@@ -491,6 +496,8 @@ def main():
                   "delta_ms_per_session_step_median": statistics.median(sess_stall_delta),
                   "delta_ms_per_session_step_p90": float(np.percentile(sess_stall_delta, 90)),
                   "session_steps_measured": len(sess_stall_delta),
+                  "delta_ms_per_session_step_ci95": delta_ci95,
+                  "delta_ci_how": f"bootstrap over the {len(per_sess)} sessions (2000 resamples)",
                   "delta_frac_of_step": statistics.mean(sess_stall_delta) / free_med,
                   "delta_ms_vs_plain_steps_same_intervals": statistics.mean(sess_ms) - statistics.median(plain_ms_steps),
                   "delta_note": "delta_* compare session steps with the checkpoint-free run measured before and after "
@@ -502,6 +509,7 @@ def main():
                       "how": "checkpoint-free intervals measured before and after the timed region, same run"},
         "d2h": {"gbs": d2h_bytes / (d2h_ms / 1e3) / 1e9 if d2h_ms > 0 else None,
                 "link_peak_gbs": link_peak, "frac": (d2h_bytes / (d2h_ms / 1e3) / 1e9) / link_peak if d2h_ms else None,
+                "frac_of_nominal_pcie5_x16": (d2h_bytes / (d2h_ms / 1e3) / 1e9) / 64.0 if d2h_ms else None,
                 "bytes_per_session": session_bytes, "link_peak_how": "best of 5 x 1 GiB cudaMemcpyAsync D2H "
                 "into pinned memory, this run"},
         "model": {"recommended_K": k_rec, "v_max_bytes_at_recommended_K": vmax_rec, "K_used": K,
