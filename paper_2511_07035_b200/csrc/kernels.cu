@@ -112,7 +112,7 @@ __global__ void __launch_bounds__(256) fused_adamw_pack_kernel(const FusedArgs a
     }
 }
 
-// ---- TMA-pipelined variant of a2 (the default for n >= kTmaMinElems) ----
+// ---- TMA-pipelined variant of a2 with STG stores (GCK_FUSED_IMPL=t; the bulk-store variant below is the default) ----
 // Persistent CTAs (default: 1 per SM, 4 stages, 16 consumer warps; GCK_TMA_CFG selects other
 // instantiations for experiments). One producer warp streams 2048-element tiles of p, m, v
 // (fp32) and g (bf16) into a kStages-deep shared-memory ring with 1-D bulk async copies
@@ -333,6 +333,198 @@ __global__ void __launch_bounds__((kCW + 2) * 32, kMinBlocks) fused_adamw_pack_t
     }
 }
 
+// ---- a2 with bulk stores too (GCK_FUSED_IMPL=x): loads AND stores through the bulk-copy engine ----
+// As fused_adamw_pack_tma_kernel, but the consumers write p', m', v', bf16(p') into a kOut-deep
+// shared-memory OUTPUT ring and a store warp bulk-copies each finished tile to global memory
+// (UBLKCP.G.S), so no STG is issued on the steady-state path. An all-bulk copy of this 8-stream
+// pattern holds 6.23 TB/s after a GEMM burst where the LDG/STG copy drops to 5.7
+// (profiles/r01_tma8_ceiling.txt): the stores no longer depend on the SM clock. The input stage
+// is not written (the pack warp still bulk-stores the pre-update bytes from it).
+constexpr int tmast_smem(int stages, int outs, int tile) { return (stages + outs) * tile * 14 + 2 * (stages + outs) * 8; }
+
+template <bool PACK, int kStages, int kOut, int kCW, int kTile>
+__global__ void __launch_bounds__((kCW + 3) * 32, 1) fused_adamw_pack_tmast_kernel(const FusedArgs a) {
+    // warps 0..kCW-1 consume; warp kCW loads; warp kCW+1 packs (session); warp kCW+2 stores
+    constexpr int kThreads = kCW * 32;
+    constexpr int kStageBytes = kTile * 14;
+    constexpr int kQ = kTile / 4 / kThreads;
+    static_assert(kQ * kThreads * 4 == kTile, "tile must split evenly");
+    extern __shared__ __align__(128) uint8_t smem[];
+    uint8_t *obuf = smem + kStages * kStageBytes;
+    uint64_t *full = reinterpret_cast<uint64_t *>(obuf + kOut * kStageBytes);
+    uint64_t *empty = full + kStages;
+    uint64_t *ofull = empty + kStages;
+    uint64_t *oempty = ofull + kOut;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint64_t n_tiles = a.n / kTile;
+    const bool skip = a.rec.skip != 0;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kCW + (PACK ? 1 : 0));
+        }
+        for (int o = 0; o < kOut; ++o) {
+            mbar_init(&ofull[o], kCW);
+            mbar_init(&oempty[o], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == kCW) {  // loads (as the STG variant)
+        if (lane == 0) {
+            uint32_t k = 0;
+            for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++k) {
+                const int s = k % kStages;
+                mbar_wait(&empty[s], ((k / kStages) & 1u) ^ 1u);
+                mbar_expect_tx(&full[s], kStageBytes);
+                uint8_t *st = smem + s * kStageBytes;
+                const uint64_t base = tile * kTile;
+                bulk_g2s(st, a.p + base, kTile * 4, &full[s]);
+                bulk_g2s(st + kTile * 4, a.m + base, kTile * 4, &full[s]);
+                bulk_g2s(st + kTile * 8, a.v + base, kTile * 4, &full[s]);
+                bulk_g2s(st + kTile * 12, a.g + base, kTile * 2, &full[s]);
+            }
+        }
+        return;
+    }
+    if (warp == kCW + 1) {  // pack (session launches only): pre-update bytes from the input stage
+        if (PACK && lane == 0) {
+            uint32_t k = 0;
+            int prev_s = -1;
+            for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++k) {
+                const int s = k % kStages;
+                mbar_wait(&full[s], (k / kStages) & 1u);
+                const uint8_t *st = smem + s * kStageBytes;
+                const uint64_t base = tile * kTile;
+                const uint64_t olo = base > a.lo ? base : a.lo;
+                const uint64_t ohi = (base + kTile) < a.hi ? (base + kTile) : a.hi;
+                const uint64_t ghi = (base + kTile) < a.ghi ? (base + kTile) : a.ghi;
+                if (olo < ohi) {
+                    const uint32_t off = (uint32_t)(olo - base), bytes = (uint32_t)(ohi - olo) * 4;
+                    bulk_s2g(a.sp + (olo - a.lo), st + off * 4, bytes);
+                    bulk_s2g(a.sm + (olo - a.lo), st + kTile * 4 + off * 4, bytes);
+                    bulk_s2g(a.sv + (olo - a.lo), st + kTile * 8 + off * 4, bytes);
+                }
+                if (base < ghi) bulk_s2g(a.sg + base, st + kTile * 12, (uint32_t)(ghi - base) * 2);
+                bulk_commit();
+                bulk_wait_read_1();
+                if (prev_s >= 0) mbar_arrive(&empty[prev_s]);
+                prev_s = s;
+            }
+            bulk_wait_read();
+            if (prev_s >= 0) mbar_arrive(&empty[prev_s]);
+            bulk_wait_all();
+        }
+        return;
+    }
+    if (warp == kCW + 2) {  // stores: finished output tiles -> global, one bulk group per tile
+        if (lane == 0) {
+            uint32_t k = 0;
+            int prev_o = -1;
+            for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++k) {
+                const int o = k % kOut;
+                mbar_wait(&ofull[o], (k / kOut) & 1u);
+                const uint8_t *ot = obuf + o * kStageBytes;
+                const uint64_t base = tile * kTile;
+                if (!skip) {
+                    bulk_s2g(a.p + base, ot, kTile * 4);
+                    bulk_s2g(a.m + base, ot + kTile * 4, kTile * 4);
+                    bulk_s2g(a.v + base, ot + kTile * 8, kTile * 4);
+                }
+                if (a.out) bulk_s2g(a.out + base, ot + kTile * 12, kTile * 2);
+                bulk_commit();
+                bulk_wait_read_1();  // the previous tile's group has read its buffer: release it
+                if (prev_o >= 0) mbar_arrive(&oempty[prev_o]);
+                prev_o = o;
+            }
+            bulk_wait_read();
+            if (prev_o >= 0) mbar_arrive(&oempty[prev_o]);
+            bulk_wait_all();  // every store performed before the CTA retires
+        }
+        return;
+    }
+    const RecF r = to_recf(a.rec);
+    const int c = threadIdx.x;
+    uint32_t k = 0;
+    for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++k) {
+        const int s = k % kStages;
+        mbar_wait(&full[s], (k / kStages) & 1u);
+        const uint8_t *st = smem + s * kStageBytes;
+        const float4 *sp = reinterpret_cast<const float4 *>(st);
+        const float4 *sm = reinterpret_cast<const float4 *>(st + kTile * 4);
+        const float4 *sv = reinterpret_cast<const float4 *>(st + kTile * 8);
+        const uint2 *sg = reinterpret_cast<const uint2 *>(st + kTile * 12);
+        float4 pq[kQ], mq[kQ], vq[kQ];
+        uint2 gq[kQ];
+#pragma unroll
+        for (int q = 0; q < kQ; ++q) {
+            pq[q] = sp[c + q * kThreads];
+            mq[q] = sm[c + q * kThreads];
+            vq[q] = sv[c + q * kThreads];
+            gq[q] = sg[c + q * kThreads];
+        }
+        // release the input stage once every lane's LDS has landed (see the STG variant)
+        uint32_t dep = 0;
+#pragma unroll
+        for (int q = 0; q < kQ; ++q)
+            dep ^= __float_as_uint(pq[q].x) ^ __float_as_uint(mq[q].x) ^ __float_as_uint(vq[q].x) ^ gq[q].x;
+        asm volatile("" : "+r"(dep));
+        __syncwarp();
+        if (lane == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            mbar_arrive(&empty[s]);
+        }
+        // compute, then write the tile's results into output buffer o once the store warp has
+        // finished reading its previous contents
+        const int o = k % kOut;
+        mbar_wait(&oempty[o], ((k / kOut) & 1u) ^ 1u);
+        uint8_t *ot = obuf + o * kStageBytes;
+        float4 *op = reinterpret_cast<float4 *>(ot);
+        float4 *om = reinterpret_cast<float4 *>(ot + kTile * 4);
+        float4 *ov = reinterpret_cast<float4 *>(ot + kTile * 8);
+        uint2 *og = reinterpret_cast<uint2 *>(ot + kTile * 12);
+#pragma unroll
+        for (int q = 0; q < kQ; ++q) {
+            float p[4] = {pq[q].x, pq[q].y, pq[q].z, pq[q].w}, m[4] = {mq[q].x, mq[q].y, mq[q].z, mq[q].w},
+                  v[4] = {vq[q].x, vq[q].y, vq[q].z, vq[q].w};
+            if (!skip) {
+                const uint32_t gb[4] = {gq[q].x & 0xFFFFu, gq[q].x >> 16, gq[q].y & 0xFFFFu, gq[q].y >> 16};
+                adamw_group_fast(p, m, v, gb, r);
+                op[c + q * kThreads] = make_float4(p[0], p[1], p[2], p[3]);
+                om[c + q * kThreads] = make_float4(m[0], m[1], m[2], m[3]);
+                ov[c + q * kThreads] = make_float4(v[0], v[1], v[2], v[3]);
+            }
+            og[c + q * kThreads] = make_uint2(pack_bf16x2(p[0], p[1]), pack_bf16x2(p[2], p[3]));
+        }
+        // generic-proxy smem writes -> visible to the async proxy (the bulk store), then arrive
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ofull[o]);
+    }
+    // ragged tail [n_tiles*kTile, n): block 0's consumers, plain loads and stores
+    if (blockIdx.x == 0) {
+        for (uint64_t e = n_tiles * kTile + (uint64_t)c; e < a.n; e += kThreads) {
+            float p = a.p[e], m = a.m[e], v = a.v[e];
+            const uint32_t g = a.g[e];
+            if (PACK) {
+                if (e >= a.lo && e < a.hi) {
+                    a.sp[e - a.lo] = p;
+                    a.sm[e - a.lo] = m;
+                    a.sv[e - a.lo] = v;
+                }
+                if (e < a.ghi) a.sg[e] = (uint16_t)g;
+            }
+            if (!skip) {
+                adamw_elem_fast(p, m, v, g, r);
+                a.p[e] = p;
+                a.m[e] = m;
+                a.v[e] = v;
+            }
+            if (a.out) a.out[e] = (uint16_t)(pack_bf16x2(p, 0.f) & 0xFFFFu);
+        }
+    }
+}
+
 __device__ __forceinline__ uint32_t part_of(const ReplayArgs &a, uint64_t e) {
     uint32_t j = 0;
     while (j + 1 < a.K && e >= a.hi[j]) ++j;
@@ -495,10 +687,35 @@ int launch_tma(const FusedArgs &a, bool pack, cudaStream_t s, int num_sms) {
     return (int)cudaGetLastError();
 }
 
+template <int S, int O, int CW, int TL = 2048>
+int launch_tmast(const FusedArgs &a, bool pack, cudaStream_t s, int num_sms) {
+    static std::atomic<uint64_t> attr_set_devices{0};  // the smem opt-in is per device
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const uint64_t bit = 1ull << (dev & 63);
+    if (!(attr_set_devices.load() & bit)) {
+        cudaFuncSetAttribute(fused_adamw_pack_tmast_kernel<true, S, O, CW, TL>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, tmast_smem(S, O, TL));
+        cudaFuncSetAttribute(fused_adamw_pack_tmast_kernel<false, S, O, CW, TL>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, tmast_smem(S, O, TL));
+        attr_set_devices.fetch_or(bit);
+    }
+    const uint64_t tiles = a.n / TL;
+    const uint64_t cap = (uint64_t)(num_sms > 0 ? num_sms : 148);
+    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, cap));
+    const unsigned block = (CW + 3) * 32;
+    if (pack)
+        fused_adamw_pack_tmast_kernel<true, S, O, CW, TL><<<grid, block, tmast_smem(S, O, TL), s>>>(a);
+    else
+        fused_adamw_pack_tmast_kernel<false, S, O, CW, TL><<<grid, block, tmast_smem(S, O, TL), s>>>(a);
+    return (int)cudaGetLastError();
+}
+
 int fused_impl_default() {
     const char *e = getenv("GCK_FUSED_IMPL");
     if (e && e[0] == 's') return 1;
     if (e && e[0] == 't') return 2;
+    if (e && e[0] == 'x') return 3;
     return 0;
 }
 
@@ -507,6 +724,27 @@ int launch_fused(const FusedArgs &a, bool pack, void *stream, int num_sms) {
     const int impl = fused_impl_default();
     const bool aligned = ((reinterpret_cast<uintptr_t>(a.p) | reinterpret_cast<uintptr_t>(a.m) |
                            reinterpret_cast<uintptr_t>(a.v) | reinterpret_cast<uintptr_t>(a.g)) & 15u) == 0;
+    const bool out_aligned = (reinterpret_cast<uintptr_t>(a.out) & 15u) == 0;
+    // default for n >= 2^18: the bulk-store variant (3 input + 3 output stages); GCK_FUSED_IMPL=t
+    // selects the STG-store TMA kernel, s the plain grid-stride kernel
+    if (aligned && out_aligned && (impl == 3 ? a.n >= 2048 : (impl == 0 && a.n >= kTmaMinElems))) {
+        const char *e = getenv("GCK_TMAST_CFG");
+        int st = 3, o = 3, cw = 16;
+        if (e) sscanf(e, "%d,%d,%d", &st, &o, &cw);
+        const int cfg = st * 100 + o * 10 + (cw == 8 ? 1 : 0);
+        switch (cfg) {
+            case 330: return launch_tmast<3, 3, 16>(a, pack, s, num_sms);
+            case 340: return launch_tmast<3, 4, 16>(a, pack, s, num_sms);
+            case 350: return launch_tmast<3, 5, 16>(a, pack, s, num_sms);
+            case 440: return launch_tmast<4, 4, 16>(a, pack, s, num_sms);
+            case 240: return launch_tmast<2, 4, 16>(a, pack, s, num_sms);
+            case 420: return launch_tmast<4, 2, 16>(a, pack, s, num_sms);
+            case 421: return launch_tmast<4, 2, 8>(a, pack, s, num_sms);
+            case 430: return launch_tmast<4, 3, 16>(a, pack, s, num_sms);
+            case 520: return launch_tmast<5, 2, 16>(a, pack, s, num_sms);
+            default: return launch_tmast<3, 3, 16>(a, pack, s, num_sms);
+        }
+    }
     if (aligned && (impl == 2 || (impl == 0 && a.n >= kTmaMinElems))) {
         const int cfg = [] {
             const char *e = getenv("GCK_TMA_CFG");

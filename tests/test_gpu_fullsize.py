@@ -119,9 +119,11 @@ def test_llama2_7b_zero1_rank_shard_fullsize(G):
     assert stats["d2h_bytes"] == oracle.session_bytes(parts)
 
 
-@pytest.mark.parametrize("cfg", ["default", "6,1,8", "3,2,16"])
-def test_tma_kernel_stress_vs_simple_kernel(G, cfg, monkeypatch):
-    """Differential stress at the bench size: the TMA-pipelined fused kernel (the default) against
+@pytest.mark.parametrize("impl,cfg", [("auto", "default"), ("t", "default"), ("t", "6,1,8"), ("t", "3,2,16"),
+                                      ("x", "4,2,16"), ("x", "3,4,16")])
+def test_tma_kernel_stress_vs_simple_kernel(G, impl, cfg, monkeypatch):
+    """Differential stress at the bench size: the TMA-pipelined fused kernels (the bulk-store default and
+    the STG-store variant, several stage configurations) against
     the plain grid-stride kernel (itself bit-exact against the oracle in test_gpu_parity), 24 steps
     plain + session, every element compared bitwise after every step. Catches shared-memory ring
     races (a stage refilled before every lane has read it) that window sampling can miss."""
@@ -130,7 +132,8 @@ def test_tma_kernel_stress_vs_simple_kernel(G, cfg, monkeypatch):
     import os
     env = dict(os.environ)
     if cfg != "default":
-        env["GCK_TMA_CFG"] = cfg
+        env["GCK_TMAST_CFG" if impl == "x" else "GCK_TMA_CFG"] = cfg
+    env["GCK_TEST_IMPL"] = impl      # auto = the default (bulk stores), t = STG stores, x = bulk stores
     code = r'''
 import os, sys, torch
 sys.path.insert(0, ".")
@@ -145,8 +148,11 @@ g = torch.empty(n, dtype=torch.int16, device="cuda")
 for s in range(1, 25):
     G.h_generate(4, g, 5, s, 0, 1, 4)
     r = G.make_step_record(0.9, 0.999, 1e-8, 0.01, 100 + s, 3e-4)
-    os.environ.pop("GCK_FUSED_IMPL", None)
-    G.adamw_step(r, *a[:3], g, a[3])                       # default launcher (TMA at this size)
+    if os.environ["GCK_TEST_IMPL"] != "auto":
+        os.environ["GCK_FUSED_IMPL"] = os.environ["GCK_TEST_IMPL"]
+    else:
+        os.environ.pop("GCK_FUSED_IMPL", None)
+    G.adamw_step(r, *a[:3], g, a[3])                       # default launcher (TMA at this size) or x
     os.environ["GCK_FUSED_IMPL"] = "simple"
     G.adamw_step(r, *b[:3], g, b[3])                       # reference: the plain grid-stride kernel
     torch.cuda.synchronize()
