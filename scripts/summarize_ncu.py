@@ -37,7 +37,7 @@ for rec in recs:
     t = float(rec["gpu__time_duration.sum"][0].replace(",", "")) * scale[rec["gpu__time_duration.sum"][1]]
     rd = float(rec["dram__bytes_read.sum"][0].replace(",", "")) * scale[rec["dram__bytes_read.sum"][1]]
     wr = float(rec["dram__bytes_write.sum"][0].replace(",", "")) * scale[rec["dram__bytes_write.sum"][1]]
-    pack = "<1>" in rec["kernel"] or "true" in rec["kernel"]
+    pack = "<1>" in rec["kernel"] or "true" in rec["kernel"] or "kernel<1," in rec["kernel"]
     alg = 28 * n
     lines.append(f"{'pack ' if pack else 'plain'} {rec['kernel'][:70]}")
     lines.append(f"   time {t * 1e6:.1f} us  dram read {rd / 1e9:.4f} GB  write {wr / 1e9:.4f} GB  "
