@@ -403,7 +403,9 @@ def main():
     plain_mean_s = statistics.mean(kern_plain) / 1e3
     achieved = plain_bytes / plain_mean_s / 1e9
     # session launches additionally write the slot (12|P_i| + 2 hi_i bytes, = the drained bytes)
-    sess_alg = args.steps * (K * plain_bytes + session_bytes)
+    # (direct / blocking staging: the D2H reads the live arrays; the kernel writes no slot bytes)
+    kern_slot_bytes = session_bytes if args.staging == "ring" else 0
+    sess_alg = args.steps * (K * plain_bytes + kern_slot_bytes)
     sess_achieved = sess_alg / (sess_kernel_ms / 1e3) / 1e9 if sess_kernel_ms > 0 and not baseline else None
     hbm_peak, peak_src = peaks()
     stall_wait_ms = (st1["stall_ms_total"] - st0["stall_ms_total"])
@@ -530,7 +532,7 @@ def main():
                      "alg_bytes_per_launch": plain_bytes, "launches": len(kern_plain),
                      "mean_launch_us": plain_mean_s * 1e6,
                      "session_launches": {"launches": sess_launches, "alg_bytes_per_launch_mean":
-                                          plain_bytes + session_bytes / K,
+                                          plain_bytes + kern_slot_bytes / K,
                                           "achieved_gbs": sess_achieved,
                                           "frac": sess_achieved / hbm_peak if sess_achieved else None}},
         "cpu_baseline": cpu,
