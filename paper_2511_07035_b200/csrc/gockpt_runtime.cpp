@@ -293,7 +293,8 @@ struct gck_ctx {
     }
     void abort_session(cudaError_t e, const char *what) {
         state = State::ABORTED;
-        last_error = std::string("checkpoint aborted: ") + what + ": " + cudaGetErrorString(e);
+        last_error = std::string("checkpoint aborted: ") + what +
+                     (e == cudaSuccess ? std::string() : std::string(": ") + cudaGetErrorString(e));
         cancel_stream();
     }
     void cancel_stream() {
@@ -1030,7 +1031,7 @@ static gck_status submit_direct(gck_ctx *c, uint32_t i, const gck_step_args *a, 
     if (i < c->K) {
         const uint64_t ghi = c->hi[i - 1];
         if (c->stream_slot_wait(i) != GCK_OK) {
-            c->abort_session(cudaSuccess, "streaming replay failed");
+            c->abort_session(cudaSuccess, "streaming replay worker failed (a drain or slice update)");
             return GCK_E_ABORTED;
         }
         if ((e = cudaEventRecord(c->ev_grad_src, s)) != cudaSuccess ||
@@ -1192,7 +1193,7 @@ gck_status gck_submit(gck_ctx *c, uint32_t part, const gck_step_args *a, void *s
         return GCK_E_ABORTED;
     }
     if (c->stream_slot_wait(i) != GCK_OK) {
-        c->abort_session(cudaSuccess, "streaming replay failed");
+        c->abort_session(cudaSuccess, "streaming replay worker failed (a drain or slice update)");
         return GCK_E_ABORTED;
     }
     if (c->cfg.timing) cudaEventRecord(c->ev_d0[i - 1], c->d2h);
