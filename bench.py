@@ -82,7 +82,7 @@ def parse():
                          "= replay-on-restore (finalize leaves the captured parts + gradient log for the "
                          "persisted file; S(T) is materialised at load); stream = streaming host replay (each slice's "
                          "update applied as it drains; gradient log = --stream-buffers recycled slices)")
-    ap.add_argument("--stream-buffers", type=int, default=0, help="streaming replay slice buffers (0 = 2)")
+    ap.add_argument("--stream-buffers", type=int, default=0, help="streaming replay slice buffers (0 = 4)")
     ap.add_argument("--replay-threads", type=int, default=0,
                     help="host replay / persist threads (0 = the host's cores divided by the local ranks)")
     ap.add_argument("--no-e2e", action="store_true")

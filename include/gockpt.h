@@ -125,7 +125,7 @@ typedef struct {
                                >= 0 binds them to that NUMA node; -1 = the GPU's own node (from its PCI
                                address; no binding if the platform reports none); -2 = no binding.
                                P:401: "28 cores per process, same NUMA domain". */
-    uint32_t stream_buffers; /* GCK_REPLAY_STREAM: gradient slice buffers B (0 -> 2); ignored otherwise */
+    uint32_t stream_buffers; /* GCK_REPLAY_STREAM: gradient slice buffers B (0 -> 4); ignored otherwise */
     uint32_t _pad_cfg;
 } gck_config;
 

@@ -250,7 +250,7 @@ struct gck_ctx {
 
     // streaming replay (GCK_REPLAY_STREAM): slices land in B recycled buffers of slice_elems
     bool stream_mode = false;
-    uint32_t B = 2;
+    uint32_t B = 4;
     uint64_t slice_elems = 0;
     uint32_t submitted = 0;        // session steps whose drain (and done event) is enqueued
     uint32_t applied = 0;          // slices whose update the stream worker has applied
@@ -718,7 +718,7 @@ gck_status gck_create(const gck_config *cfg_in, const gck_hparams *hp, const gck
             delete c;
             return set_tls(GCK_E_INVALID, "stream_buffers must be <= 64");
         }
-        c->B = cfg.stream_buffers ? cfg.stream_buffers : 2;
+        c->B = cfg.stream_buffers ? cfg.stream_buffers : 4;  // B=4: no host-side starvation at 13B/K=16 (r01_stream_13b_k16.txt)
         c->slice_elems = align_up(cfg.n, 128);
         glog_max = (uint64_t)c->B * c->slice_elems;
     }

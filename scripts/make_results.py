@@ -114,8 +114,9 @@ to the GPU's own synchronous snapshot over all elements and to the oracle on sam
   virtio disk (GPT-2 shard 0.77 s / 0.54 s; 7B rank shard 5.2 s / 3.2 s).
 - **Replay modes** (`{tag}_replay_modes.txt`, `{tag}_persist_modes.txt`): streaming host replay
   (B = 2 recycled slice buffers: pinned arena 16n instead of 19n) ratio 0.9967 vs 0.9959 batch, D2H
-  56.0 vs 56.8 GB/s on GPT-2/K=8, but at 13B rank-of-8/K=16 it costs D2H bandwidth (35.7 vs 52.6 GB/s)
-  and 8.2 vs 1.4 ms stall per session step (`{tag}_stream_13b_k16.txt`); replay-on-restore: finalize 3 ms instead of 31 ms, file 2.36 vs 1.49 GB,
+  56.0 vs 56.8 GB/s on GPT-2/K=8; at 13B rank-of-8/K=16 B=2 starves the GPU queue (5–8 ms stall per
+  session step) while the default B=4 (arena 20n instead of 27n) stalls 1.0 ms, on par with the batch
+  replay (`{tag}_stream_13b_k16.txt`); replay-on-restore: finalize 3 ms instead of 31 ms, file 2.36 vs 1.49 GB,
   persist 1.19 vs 0.76 s, cold restore (GPU replay in place) 1.46 vs 0.54 s; restored bytes
   identical (CRC) in every mode.
 - **Sanitizers** (`{tag}_sanitizers.txt`, `{tag}_host_sanitizers.txt`, `{tag}_gpu_tsan.txt`): compute-sanitizer
