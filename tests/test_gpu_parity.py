@@ -392,6 +392,7 @@ def test_deferred_replay_session_restore(G, tmp_path, n, K, A, staging):
 # ---------------------------------------------------------------- a5 streaming host replay
 @pytest.mark.parametrize("n,K,A,B,staging,copy", [(1 << 20, 4, 1024, 2, "ring", "ce"),
                                                   (1_000_003, 8, 1024, 2, "ring", "ce"),
+                                                  (1_000_003, 8, 1024, 0, "ring", "ce"),     # default B (4)
                                                   (1_000_003, 8, 1024, 1, "ring", "zerocopy"),
                                                   (300_007, 6, 8, 3, "direct", "ce"),
                                                   (5000, 2, 8, 2, "ring", "ce"),
