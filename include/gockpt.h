@@ -125,8 +125,13 @@ typedef struct {
                                >= 0 binds them to that NUMA node; -1 = the GPU's own node (from its PCI
                                address; no binding if the platform reports none); -2 = no binding.
                                P:401: "28 cores per process, same NUMA domain". */
-    uint32_t stream_buffers; /* GCK_REPLAY_STREAM: gradient slice buffers B (0 -> 4); ignored otherwise */
-    uint32_t _pad_cfg;
+    uint32_t stream_buffers; /* GCK_REPLAY_STREAM: gradient slice buffers B (0 -> min(4, k_max - 1)); ignored
+                                otherwise */
+    int32_t verify_drain;   /* 1: verify every drained slice (a3) — a checksum kernel reads each section on
+                               the D2H stream right before its copy (the bytes the copy reads), the host
+                               recomputes the checksum of the landed bytes before the replay uses them
+                               (A = sum w_i, B = sum (i+1) w_i mod 2^64 over 32-bit words); a mismatch
+                               voids the session with GCK_E_CORRUPT. 0: no verification */
 } gck_config;
 
 /* Caller-owned device tensors (PyTorch owns them; they must outlive the context). */
@@ -202,6 +207,8 @@ typedef struct {
     double auto_step_ms;           /* step time the last automatic K used (0: not measured) */
     double auto_link_gbs;          /* link rate the last automatic K used */
     double last_stream_wait_ms;    /* GCK_REPLAY_STREAM: host time gck_submit blocked on slice-buffer reuse */
+    double last_verify_ms;         /* batch replay: host time of the last session's completeness check and
+                                      drain verification (cfg.verify_drain) before the replay */
 } gck_stats;
 
 /* ---- context lifecycle -------------------------------------------------- */
@@ -241,7 +248,11 @@ gck_status gck_begin_checkpoint(gck_ctx *ctx, uint64_t t0, uint32_t K);
  * Errors: INVALID, PROTOCOL, STALE, CUDA (kernel launch failure poisons ctx),
  * ABORTED (the checkpoint path failed — now or earlier in this session; the update still ran
  * as a plain step, the session is void: gck_finalize reports ABORTED, gck_begin_checkpoint
- * starts a new one). Test hook: GCK_FAULT_DRAIN=<i> fails the drain of session step i. */
+ * starts a new one). Test hooks (environment, read at gck_begin_checkpoint; i = session step):
+ * GCK_FAULT_DRAIN=<i> fails the drain enqueue of step i (ABORTED here); GCK_FAULT_DROP_SLICE=<i>
+ * silently skips step i's drain (gck_finalize then reports INCOMPLETE); GCK_FAULT_FLIP=<i> flips
+ * one landed byte of step i's state part on the host before verification (gck_finalize reports
+ * CORRUPT with cfg.verify_drain, else the checkpoint differs from S(T)). */
 gck_status gck_submit(gck_ctx *ctx, uint32_t part, const gck_step_args *args, void *stream);
 
 /* Direct staging: make `stream` wait until the gradient slice of the latest session step has
@@ -258,7 +269,12 @@ gck_status gck_wait_drained(gck_ctx *ctx);
 gck_status gck_get_staged(gck_ctx *ctx, gck_staged *out);
 
 /* Block until the checkpoint is consistent (drains complete, replay done, a5/a6)
- * and describe it. Errors: PROTOCOL (part K not yet submitted), ABORTED, INCOMPLETE. */
+ * and describe it. Before the replay uses any slice, every session step must have drained its
+ * state part and gradient slice, else INCOMPLETE (a missing slice is never replayed
+ * around); with cfg.verify_drain every landed section must match the checksum of the staged
+ * bytes, else CORRUPT. Both void the session (state as after ABORTED: gck_release, then a new
+ * gck_begin_checkpoint; training is unaffected).
+ * Errors: PROTOCOL (part K not yet submitted), ABORTED, INCOMPLETE, CORRUPT. */
 gck_status gck_finalize(gck_ctx *ctx, gck_checkpoint *out);
 
 /* Non-blocking finalize: GCK_E_BUSY while drains/replay are still running. */
@@ -317,6 +333,12 @@ gck_status gck_adamw_step(const gck_step_record *rec, uint64_t n, float *d_maste
  * both 16-B aligned). Async. Used by the host-link bandwidth sweep (BASELINE config 5). */
 gck_status gck_d2h_copy(void *dst_host, const void *src_dev, uint64_t bytes, int32_t mode, uint64_t chunk_bytes,
                         uint32_t zc_ctas, void *stream);
+
+/* a3 drain verification, host side (the definition cfg.verify_drain uses on both sides): over the
+ * little-endian 32-bit words w_0..w_{W-1} of [host, host+bytes) (a partial last word zero-padded),
+ * out_ab[0] = A = sum w_i, out_ab[1] = B = sum (i+1) w_i, both mod 2^64. Host-only; `threads`
+ * threads (0 = all cores of the affinity mask). Errors: INVALID (NULL pointers). */
+gck_status gck_checksum(const void *host, uint64_t bytes, int32_t threads, uint64_t *out_ab);
 
 /* ---- NEXT-1: persistence and restore (§4.3.2, §4.4.1, §4.4.3) -------- */
 

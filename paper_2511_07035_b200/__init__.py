@@ -11,7 +11,7 @@ binding without the built library raises.
 """
 
 from .gockpt import (GoCkpt, HostCheckpoint, make_step_record, plan_parts, replay_host, replay_device,
-                     adamw_step, h_generate, d2h_copy, device_count,
+                     adamw_step, h_generate, d2h_copy, checksum, device_count,
                      write_checkpoint, write_checkpoint_log, read_header, read_log_header, load_checkpoint,
                      load_checkpoint_range, recommend_k,
                      ring_bytes_required, GEN_MASTER, GEN_EXP_AVG, GEN_EXP_AVG_SQ, GEN_GRAD)
@@ -19,7 +19,7 @@ from ._lib import GckError, lib, LIB_PATH
 from .optim import CheckpointedAdamW
 
 __all__ = ["GoCkpt", "CheckpointedAdamW", "HostCheckpoint", "make_step_record", "plan_parts", "replay_host", "replay_device",
-           "adamw_step", "h_generate", "d2h_copy", "device_count",
+           "adamw_step", "h_generate", "d2h_copy", "checksum", "device_count",
            "write_checkpoint", "write_checkpoint_log", "read_header", "read_log_header", "load_checkpoint",
            "load_checkpoint_range", "recommend_k",
            "ring_bytes_required", "GckError", "lib", "LIB_PATH",

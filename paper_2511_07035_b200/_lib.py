@@ -39,7 +39,7 @@ class Config(C.Structure):
                 ("ring_slots", C.c_uint32), ("copy_mode", C.c_int32), ("chunk_bytes", C.c_uint64),
                 ("zc_ctas", C.c_uint32), ("replay_mode", C.c_int32), ("replay_threads", C.c_int32),
                 ("timing", C.c_int32), ("eager_replay", C.c_int32), ("staging", C.c_int32),
-                ("numa_node", C.c_int32), ("stream_buffers", C.c_uint32), ("_pad_cfg", C.c_uint32)]
+                ("numa_node", C.c_int32), ("stream_buffers", C.c_uint32), ("verify_drain", C.c_int32)]
 
 
 class Tensors(C.Structure):
@@ -80,7 +80,7 @@ class Stats(C.Structure):
                 ("last_finalize_wait_ms", C.c_double), ("last_session_d2h_bytes", C.c_uint64),
                 ("gpu_launches", C.c_uint64), ("replay_threads", C.c_int32), ("numa_node", C.c_int32),
                 ("last_session_k", C.c_uint32), ("_pad2", C.c_uint32), ("auto_step_ms", C.c_double),
-                ("auto_link_gbs", C.c_double), ("last_stream_wait_ms", C.c_double)]
+                ("auto_link_gbs", C.c_double), ("last_stream_wait_ms", C.c_double), ("last_verify_ms", C.c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_ if not k.startswith("_")}
@@ -140,6 +140,7 @@ SIGNATURES = {
     "gck_h_generate": (C.c_int, [C.c_int32, C.c_int32, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64,
                                  C.c_uint32, P, P]),
     "gck_d2h_copy": (C.c_int, [P, P, C.c_uint64, C.c_int32, C.c_uint64, C.c_uint32, P]),
+    "gck_checksum": (C.c_int, [P, C.c_uint64, C.c_int32, U64P]),
     "gck_write_checkpoint": (C.c_int, [C.c_char_p, C.POINTER(FileHeader), P, P, P, C.c_int32, C.c_char_p,
                                        C.POINTER(PersistStats)]),
     "gck_read_header": (C.c_int, [C.c_char_p, C.POINTER(FileHeader)]),

@@ -277,6 +277,14 @@ struct gck_ctx {
     std::string persist_error;
     bool persist_started = false;
 
+    // drain verification (cfg.verify_drain) and the session's fault hooks
+    bool verify = false;
+    unsigned long long *dsum = nullptr;  // device: [GCK_K_LIMIT][4 sections][A, B] of the staged bytes
+    unsigned long long *hsum = nullptr;  // pinned host mirror, copied on the D2H stream before the drain
+    uint64_t state_mask = 0, grad_mask = 0;  // session steps whose state part / gradient slice drained
+    uint32_t fault_drop = 0, fault_flip = 0;  // GCK_FAULT_DROP_SLICE / GCK_FAULT_FLIP (read at begin)
+    std::string worker_error;                 // why the worker failed (set before worker_done)
+
     // bias-correction power cache (left-to-right binary64 running products)
     uint64_t pow_t = 0;
     double pow1 = 1.0, pow2 = 1.0;
@@ -291,8 +299,10 @@ struct gck_ctx {
         poisoned = true;
         return fail(GCK_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
     }
+    gck_status abort_status = GCK_E_ABORTED;  // what gck_finalize reports for an aborted session
     void abort_session(cudaError_t e, const char *what) {
         state = State::ABORTED;
+        abort_status = GCK_E_ABORTED;
         last_error = std::string("checkpoint aborted: ") + what +
                      (e == cudaSuccess ? std::string() : std::string(": ") + cudaGetErrorString(e));
         cancel_stream();
@@ -301,6 +311,42 @@ struct gck_ctx {
         std::lock_guard<std::mutex> lk(mu);
         stream_cancel = true;
         cv.notify_all();
+    }
+
+    // Session step i had its state part (and, for i < K, its gradient slice) drained. The masks are
+    // written by the submitting thread before it publishes the step (finish_session_step, under
+    // mu) and only read here, by the worker after that publication.
+    gck_status check_step(uint32_t i) {
+        const uint64_t bit = 1ull << (i - 1);
+        if ((state_mask & bit) && (i == K || (grad_mask & bit))) return GCK_OK;
+        worker_error = "session step " + std::to_string(i) +
+                       (!(state_mask & bit) ? " (state part)" : " (gradient slice)") +
+                       " never drained: the checkpoint is incomplete and discarded";
+        return GCK_E_INCOMPLETE;
+    }
+
+    // Host side of the drain verification for session step i (after done[i-1]): the checksums of
+    // the landed bytes against the device checksums of the staged bytes (taken on the D2H stream
+    // right before the copy). GCK_FAULT_FLIP=<i> corrupts one landed byte first (test hook).
+    gck_status verify_step(uint32_t i) {
+        const uint64_t lo = this->lo[i - 1], pe = hi[i - 1] - lo, ghi = (i < K) ? hi[i - 1] : 0;
+        if (fault_flip == i) reinterpret_cast<uint8_t *>(h_master + lo)[pe * 2] ^= 0x10u;
+        if (!verify) return GCK_OK;
+        const void *sec[4] = {h_master + lo, h_m + lo, h_v + lo, glog[i - 1]};
+        const uint64_t bytes[4] = {pe * 4, pe * 4, pe * 4, ghi * 2};
+        static const char *names[4] = {"master", "exp_avg", "exp_avg_sq", "gradient"};
+        for (int k = 0; k < 4; ++k) {
+            if (!bytes[k]) continue;
+            uint64_t a = 0, b = 0;
+            gck::checksum_host(sec[k], bytes[k], &a, &b, cfg.replay_threads, numa >= 0 ? &numa_cpus : nullptr);
+            const unsigned long long *d = hsum + (uint64_t)(i - 1) * 8 + 2 * k;
+            if (a != d[0] || b != d[1]) {
+                worker_error = "drain verification: session step " + std::to_string(i) + " " + names[k] +
+                               " section differs from the staged bytes (checksum mismatch)";
+                return GCK_E_CORRUPT;
+            }
+        }
+        return GCK_OK;
     }
 
     // a5, streaming (GCK_REPLAY_STREAM): as soon as session step i+1 has drained (part i+1 at
@@ -327,6 +373,7 @@ struct gck_ctx {
                     break;
                 }
                 const auto r0 = std::chrono::steady_clock::now();
+                if ((st = check_step(i + 1)) != GCK_OK || (st = verify_step(i + 1)) != GCK_OK) break;
                 const gck_step_record r2[2] = {recs[i], recs[i]};
                 const uint64_t lo2[2] = {0, hi[i]}, hi2[2] = {hi[i], cfg.n};
                 const uint16_t *g2[2] = {glog[i], nullptr};
@@ -343,6 +390,7 @@ struct gck_ctx {
                 if (stream_cancel) st = GCK_E_ABORTED;
                 lk.unlock();
                 if (st == GCK_OK && cudaEventSynchronize(done[K - 1]) != cudaSuccess) st = GCK_E_ABORTED;
+                if (st == GCK_OK && (st = check_step(K)) == GCK_OK) st = verify_step(K);
             }
         }
         const double ms =
@@ -369,6 +417,23 @@ struct gck_ctx {
         stats.last_stream_wait_ms +=
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count();
         return ok ? GCK_OK : GCK_E_ABORTED;
+    }
+
+    // The streaming worker stopped (a slice missing or corrupt, a failed drain): void the session;
+    // finalize reports the worker's own status.
+    void stream_worker_failed() {
+        gck_status ws;
+        std::string we;
+        {
+            std::lock_guard<std::mutex> lk(mu);
+            ws = worker_status;
+            we = worker_error;
+        }
+        abort_session(cudaSuccess, "streaming replay worker failed (a drain or slice update)");
+        if (ws == GCK_E_INCOMPLETE || ws == GCK_E_CORRUPT) {
+            abort_status = ws;
+            last_error = we;
+        }
     }
 
     void record_for(uint64_t adam_t, double lr, double gs, int32_t skip, gck_step_record *out) {
@@ -460,6 +525,14 @@ struct gck_ctx {
                 // time of finalize latency
                 cudaError_t e = cudaEventSynchronize(done[K - 1]);
                 if (e != cudaSuccess) st = GCK_E_ABORTED;
+            }
+            // a slice that never drained voids the session (GCK_E_INCOMPLETE); drain verification
+            if (st == GCK_OK && !replayed) {
+                const auto v0 = std::chrono::steady_clock::now();
+                for (uint32_t i = 1; i <= K && st == GCK_OK; ++i) st = check_step(i);
+                for (uint32_t i = 1; i <= K && st == GCK_OK; ++i) st = verify_step(i);
+                stats.last_verify_ms =
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - v0).count();
             }
             // replay-on-restore: the stale parts stay as captured; the load replays them
             if (st == GCK_OK && !replayed && cfg.replay_mode != GCK_REPLAY_DEFERRED) {
@@ -718,8 +791,19 @@ gck_status gck_create(const gck_config *cfg_in, const gck_hparams *hp, const gck
             delete c;
             return set_tls(GCK_E_INVALID, "stream_buffers must be <= 64");
         }
-        c->B = cfg.stream_buffers ? cfg.stream_buffers : 4;  // B=4: no host-side starvation at 13B/K=16 (r01_stream_13b_k16.txt)
-        c->slice_elems = align_up(cfg.n, 128);
+        // B=4 by default: no host-side starvation at 13B/K=16 (r01_stream_13b_k16.txt); a session
+        // has at most K-1 slices in flight, so buffers beyond k_max-1 would never be used
+        const uint64_t U = (cfg.n + cfg.part_align - 1) / cfg.part_align;
+        const uint32_t kmax_eff = (uint32_t)std::min<uint64_t>(cfg.k_max, U);
+        c->B = cfg.stream_buffers ? cfg.stream_buffers : 4;
+        c->B = std::min<uint32_t>(c->B, std::max<uint32_t>(1, kmax_eff - 1));
+        uint64_t largest = 0;  // the largest gradient slice G[0:hi_{K-1}] over K in [k_min, k_max]
+        for (uint32_t K = std::max<uint32_t>(2, cfg.k_min); K <= kmax_eff; ++K) {
+            uint64_t lo[GCK_K_LIMIT], hi[GCK_K_LIMIT];
+            plan_parts(cfg.n, K, cfg.part_align, lo, hi);
+            largest = std::max(largest, hi[K - 2]);
+        }
+        c->slice_elems = align_up(largest, 128);
         glog_max = (uint64_t)c->B * c->slice_elems;
     }
     c->glog_elems_cap = glog_max;
@@ -793,6 +877,17 @@ gck_status gck_create(const gck_config *cfg_in, const gck_hparams *hp, const gck
         gck_destroy(c);
         return set_tls(GCK_E_CUDA, "stream/event creation failed");
     }
+    c->verify = cfg.verify_drain != 0;
+    if (c->verify) {
+        const size_t sb = sizeof(unsigned long long) * 8 * GCK_K_LIMIT;
+        if (cudaMalloc((void **)&c->dsum, sb) != cudaSuccess ||
+            cudaHostAlloc((void **)&c->hsum, sb, cudaHostAllocPortable) != cudaSuccess) {
+            cudaGetLastError();
+            gck_destroy(c);
+            return set_tls(GCK_E_NOMEM, "drain verification buffers");
+        }
+        std::memset(c->hsum, 0, sb);
+    }
     c->stats.replay_threads = cfg.replay_threads > 0 ? cfg.replay_threads
                               : (c->numa >= 0 ? CPU_COUNT(&c->numa_cpus) : gck::default_threads());
     *out = c;
@@ -826,6 +921,8 @@ gck_status gck_destroy(gck_ctx *c) {
             cudaStreamDestroy(c->rstream);
         }
         if (c->rscratch) cudaFree(c->rscratch);
+        if (c->dsum) cudaFree(c->dsum);
+        if (c->hsum) cudaFreeHost(c->hsum);
         if (c->ring && c->ring_owned) cudaFree(c->ring);
         if (c->arena && c->arena_registered) {
             cudaHostUnregister(c->arena);
@@ -840,6 +937,8 @@ gck_status gck_destroy(gck_ctx *c) {
 
 static int drain_sections(int mode, const void *const *src, void *const *dst, void *const *dst_dev,
                           const uint64_t *bytes, int count, uint64_t chunk_bytes, uint32_t ctas, cudaStream_t s);
+static gck_status enqueue_checksum(gck_ctx *c, uint32_t i, const void *const *src, const uint64_t *bytes, int count,
+                                   int sec0);
 
 // Direct staging: D2H of part i's state [lo_i, hi_i) straight from the live arrays on the
 // side stream (ordered by the caller after the update that produced S(t0+i-1)).
@@ -850,13 +949,21 @@ static cudaError_t enqueue_state_copy(gck_ctx *c, uint32_t i) {
     void *dd[3];
     for (int k = 0; k < 3; ++k) dd[k] = c->arena_dev + ((char *)dst[k] - c->arena);
     const uint64_t bytes[3] = {pe * 4, pe * 4, pe * 4};
-    if (c->cfg.timing) cudaEventRecord(c->ev_d0[i - 1], c->d2h);
-    const int r = drain_sections(c->cfg.copy_mode, src, dst, dd, bytes, 3, c->cfg.chunk_bytes, c->cfg.zc_ctas, c->d2h);
-    if (r < 0) return cudaErrorUnknown;
-    c->stats.gpu_launches += (uint64_t)r;
-    if (c->cfg.timing) cudaEventRecord(c->ev_d1[i - 1], c->d2h);
-    c->stats.d2h_bytes += 3 * pe * 4;
-    c->stats.last_session_d2h_bytes += 3 * pe * 4;
+    if (c->fault_drop != i) {  // test hook GCK_FAULT_DROP_SLICE: part i silently never drains
+        if (enqueue_checksum(c, i, src, bytes, 3, 0) != GCK_OK) return cudaErrorUnknown;
+        if (c->cfg.timing) cudaEventRecord(c->ev_d0[i - 1], c->d2h);
+        const int r =
+            drain_sections(c->cfg.copy_mode, src, dst, dd, bytes, 3, c->cfg.chunk_bytes, c->cfg.zc_ctas, c->d2h);
+        if (r < 0) return cudaErrorUnknown;
+        c->stats.gpu_launches += (uint64_t)r;
+        if (c->cfg.timing) cudaEventRecord(c->ev_d1[i - 1], c->d2h);
+        c->stats.d2h_bytes += 3 * pe * 4;
+        c->stats.last_session_d2h_bytes += 3 * pe * 4;
+        c->state_mask |= 1ull << (i - 1);
+    } else if (c->cfg.timing) {
+        cudaEventRecord(c->ev_d0[i - 1], c->d2h);
+        cudaEventRecord(c->ev_d1[i - 1], c->d2h);
+    }
     return cudaEventRecord(c->ev_state_copied[i - 1], c->d2h);
 }
 
@@ -920,6 +1027,14 @@ gck_status gck_begin_checkpoint(gck_ctx *c, uint64_t t0, uint32_t K) {
     }
     if (off > c->glog_elems_cap) return c->fail(GCK_E_INVALID, "gradient log capacity exceeded");
     c->stats.last_session_d2h_bytes = 0;
+    c->state_mask = c->grad_mask = 0;
+    c->worker_error.clear();
+    c->K = K;  // the drain/verify paths below read K
+    {  // test hooks (session step numbers, 1-based): a slice that never drains / one corrupted landed byte
+        const char *d = getenv("GCK_FAULT_DROP_SLICE"), *f = getenv("GCK_FAULT_FLIP");
+        c->fault_drop = d ? (uint32_t)strtoul(d, nullptr, 10) : 0;
+        c->fault_flip = f ? (uint32_t)strtoul(f, nullptr, 10) : 0;
+    }
     if (c->direct) {
         // part 1 = S(t0): copy it once the last update has finished (it overlaps step t0+1's F/B)
         DeviceGuard g(c->cfg.device);
@@ -983,9 +1098,30 @@ static bool drain_fault(uint32_t i) {
     return e && (uint32_t)strtoul(e, nullptr, 10) == i;
 }
 
+// Drain verification, device side: checksums of the sections about to be copied, on the D2H
+// stream right before the copy (so they see exactly the bytes the copy reads), into dsum[i-1]
+// sections sec0.., then into the pinned mirror hsum (read by verify_step after done[i-1]).
+static gck_status enqueue_checksum(gck_ctx *c, uint32_t i, const void *const *src, const uint64_t *bytes, int count,
+                                   int sec0) {
+    if (!c->verify) return GCK_OK;
+    ZcArgs z;
+    std::memset(&z, 0, sizeof(z));
+    for (int k = 0; k < count; ++k) {
+        z.src[k] = src[k];
+        z.bytes[k] = bytes[k];
+    }
+    z.count = count;
+    unsigned long long *d = c->dsum + (uint64_t)(i - 1) * 8 + 2 * sec0, *h = c->hsum + (uint64_t)(i - 1) * 8 + 2 * sec0;
+    if (gck::launch_checksum(z, d, c->d2h, c->num_sms)) return GCK_E_ABORTED;
+    if (cudaMemcpyAsync(h, d, 16ull * count, cudaMemcpyDeviceToHost, c->d2h) != cudaSuccess) return GCK_E_ABORTED;
+    c->stats.gpu_launches++;
+    return GCK_OK;
+}
+
 static gck_status enqueue_drain(gck_ctx *c, uint32_t i, const SlotLayout &L, char *slot) {
     // slot -> host ckpt arrays at offset lo_i, gradient -> glog[i]
     if (drain_fault(i)) return GCK_E_ABORTED;
+    if (c->fault_drop == i) return GCK_OK;  // test hook: the slice silently never drains
     const uint64_t lo = c->lo[i - 1], pe = c->hi[i - 1] - lo;
     const uint64_t ghi = (i < c->K) ? c->hi[i - 1] : 0;
     const void *src[4] = {slot, slot + L.off_m, slot + L.off_v, slot + L.off_g};
@@ -1000,6 +1136,8 @@ static gck_status enqueue_drain(gck_ctx *c, uint32_t i, const SlotLayout &L, cha
     const uint64_t tot = bytes[0] + bytes[1] + bytes[2] + bytes[3];
     c->stats.d2h_bytes += tot;
     c->stats.last_session_d2h_bytes += tot;
+    c->state_mask |= 1ull << (i - 1);
+    if (ghi) c->grad_mask |= 1ull << (i - 1);
     return GCK_OK;
 }
 
@@ -1031,7 +1169,7 @@ static gck_status submit_direct(gck_ctx *c, uint32_t i, const gck_step_args *a, 
     if (i < c->K) {
         const uint64_t ghi = c->hi[i - 1];
         if (c->stream_slot_wait(i) != GCK_OK) {
-            c->abort_session(cudaSuccess, "streaming replay worker failed (a drain or slice update)");
+            c->stream_worker_failed();
             return GCK_E_ABORTED;
         }
         if ((e = cudaEventRecord(c->ev_grad_src, s)) != cudaSuccess ||
@@ -1043,18 +1181,27 @@ static gck_status submit_direct(gck_ctx *c, uint32_t i, const gck_step_args *a, 
         void *dst[1] = {c->glog[i - 1]};
         void *dd[1] = {c->arena_dev + ((char *)c->glog[i - 1] - c->arena)};
         const uint64_t bytes[1] = {ghi * 2};
+        const bool dropped = c->fault_drop == i;  // test hook: the slice silently never drains
+        if (!dropped && enqueue_checksum(c, i, src, bytes, 1, 3) != GCK_OK) {
+            c->abort_session(cudaGetLastError(), "direct: drain verification checksum");
+            return GCK_E_ABORTED;
+        }
         if (c->cfg.timing) cudaEventRecord(c->ev_g0[i - 1], c->d2h);
-        const int r = drain_sections(c->cfg.copy_mode, src, dst, dd, bytes, 1, c->cfg.chunk_bytes, c->cfg.zc_ctas,
-                                     c->d2h);
+        const int r = dropped ? 0
+                              : drain_sections(c->cfg.copy_mode, src, dst, dd, bytes, 1, c->cfg.chunk_bytes,
+                                               c->cfg.zc_ctas, c->d2h);
         if (c->cfg.timing) cudaEventRecord(c->ev_g1[i - 1], c->d2h);
         if (r < 0 || cudaEventRecord(c->ev_grad_copied, c->d2h) != cudaSuccess) {
             c->abort_session(cudaGetLastError(), "direct: gradient copy");
             return GCK_E_ABORTED;
         }
         c->grad_copy_recorded = true;
-        c->stats.gpu_launches += (uint64_t)r;
-        c->stats.d2h_bytes += ghi * 2;
-        c->stats.last_session_d2h_bytes += ghi * 2;
+        if (!dropped) {
+            c->stats.gpu_launches += (uint64_t)r;
+            c->stats.d2h_bytes += ghi * 2;
+            c->stats.last_session_d2h_bytes += ghi * 2;
+            c->grad_mask |= 1ull << (i - 1);
+        }
     }
     // a4 (direct): the update may not overwrite part i before its state copy has been taken;
     // paper-faithful GoCkpt additionally blocks until this step's gradient slice is on the host
@@ -1193,8 +1340,16 @@ gck_status gck_submit(gck_ctx *c, uint32_t part, const gck_step_args *a, void *s
         return GCK_E_ABORTED;
     }
     if (c->stream_slot_wait(i) != GCK_OK) {
-        c->abort_session(cudaSuccess, "streaming replay worker failed (a drain or slice update)");
+        c->stream_worker_failed();
         return GCK_E_ABORTED;
+    }
+    if (c->fault_drop != i) {
+        const void *src[4] = {slot, slot + L.off_m, slot + L.off_v, slot + L.off_g};
+        const uint64_t pe = hi - lo, bytes[4] = {pe * 4, pe * 4, pe * 4, ghi * 2};
+        if (enqueue_checksum(c, i, src, bytes, ghi ? 4 : 3, 0) != GCK_OK) {
+            c->abort_session(cudaGetLastError(), "drain verification checksum");
+            return GCK_E_ABORTED;
+        }
     }
     if (c->cfg.timing) cudaEventRecord(c->ev_d0[i - 1], c->d2h);
     if (enqueue_drain(c, i, L, slot) != GCK_OK) {
@@ -1245,7 +1400,7 @@ gck_status gck_get_staged(gck_ctx *c, gck_staged *out) {
 
 static gck_status finalize_impl(gck_ctx *c, gck_checkpoint *out, bool block) {
     if (!c || !out) return set_tls(GCK_E_INVALID, "null argument");
-    if (c->state == State::ABORTED) return c->fail(GCK_E_ABORTED, c->last_error);
+    if (c->state == State::ABORTED) return c->fail(c->abort_status, c->last_error);
     if (c->state == State::ACTIVE || c->state == State::IDLE)
         return c->fail(GCK_E_PROTOCOL, "finalize before part K was submitted");
     if (c->state == State::DRAINING) {
@@ -1268,7 +1423,8 @@ static gck_status finalize_impl(gck_ctx *c, gck_checkpoint *out, bool block) {
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
         if (c->worker_status != GCK_OK) {
             c->state = State::ABORTED;
-            return c->fail(c->worker_status, "replay or drain failed");
+            c->abort_status = c->worker_status;
+            return c->fail(c->worker_status, c->worker_error.empty() ? "replay or drain failed" : c->worker_error);
         }
         {
             DeviceGuard g(c->cfg.device);
@@ -1293,6 +1449,14 @@ gck_status gck_release(gck_ctx *c) {
     if (!c) return set_tls(GCK_E_INVALID, "null ctx");
     if (c->state != State::READY && c->state != State::ABORTED)
         return c->fail(GCK_E_PROTOCOL, "release without a finalized checkpoint");
+    if (c->state == State::ABORTED) {  // nothing of the aborted session may still write the arena
+        c->cancel_stream();
+        c->join_worker();
+        DeviceGuard g(c->cfg.device);
+        cudaStreamSynchronize(c->d2h);
+        if (c->rstream) cudaStreamSynchronize(c->rstream);
+        cudaGetLastError();
+    }
     c->join_worker();
     c->join_persist();  // the next session may not begin before this checkpoint is durable
     c->state = State::IDLE;
@@ -1500,6 +1664,11 @@ gck_status gck_restore(gck_ctx *c, const char *path, void *stream, gck_file_head
     if (!c || !path) return set_tls(GCK_E_INVALID, "null argument");
     if (c->state != State::IDLE) return c->fail(GCK_E_PROTOCOL, "restore while a session or checkpoint is live");
     c->join_persist();
+    c->join_worker();
+    {  // the load overwrites the pinned arena: no drain of an earlier session may still be landing in it
+        DeviceGuard g(c->cfg.device);
+        if (cudaStreamSynchronize(c->d2h) != cudaSuccess) cudaGetLastError();
+    }
     float *dst[3] = {c->h_master, c->h_m, c->h_v};
     std::string err;
     gck_file_header h;
@@ -1557,6 +1726,12 @@ gck_status gck_restore(gck_ctx *c, const char *path, void *stream, gck_file_head
     if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return c->cuda_fail(e, "restore");
     c->count_known = h.adam_t;
     if (out) *out = h;
+    return GCK_OK;
+}
+
+gck_status gck_checksum(const void *host, uint64_t bytes, int32_t threads, uint64_t *out_ab) {
+    if (!out_ab || (!host && bytes)) return set_tls(GCK_E_INVALID, "null argument");
+    gck::checksum_host(host, bytes, &out_ab[0], &out_ab[1], threads, nullptr);
     return GCK_OK;
 }
 

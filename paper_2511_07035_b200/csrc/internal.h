@@ -36,6 +36,19 @@ struct ReplayArgs {
     gck_step_record rec[GCK_K_LIMIT];
 };
 
+// The replay kernel's compacted plan (built from ReplayArgs by launch_replay): the K-1 stale part
+// ends and, in ascending order, only the non-skipped StepRecords with their gradient slices;
+// part j (0-based) needs compacted records first[j] .. nact-1.
+struct ReplayPlan {
+    float *p, *m, *v;
+    uint64_t n_replay;
+    uint32_t nact, _pad;
+    uint64_t hi[GCK_K_LIMIT];
+    uint32_t first[GCK_K_LIMIT];
+    const uint16_t *glog[GCK_K_LIMIT];
+    gck_step_record rec[GCK_K_LIMIT];
+};
+
 // Up to 4 (src, dst, bytes) sections drained by the zero-copy kernel (a3 variant).
 struct ZcArgs {
     const void *src[4];
@@ -52,6 +65,10 @@ int launch_generate(int kind, int mode, uint64_t seed, uint64_t step, uint64_t o
                     uint32_t zero_per_256, void *out, void *stream, int num_sms);
 
 int launch_cast_bf16(const float *src, uint16_t *dst, uint64_t n, void *stream, int num_sms);
+// Drain verification: d_out[2s], d_out[2s+1] = (A, B) checksums of section s (checksum_host's
+// definition), zeroed first; async on stream.
+int launch_checksum(const ZcArgs &a, unsigned long long *d_out, void *stream, int num_sms);
+int launch_flip_byte(void *dev_byte, void *stream);  // test hook: XOR one device byte
 
 // Persistence (persist.cpp).
 // The replay log a version-2 (replay-on-restore) file carries: the session plan, its K
@@ -94,5 +111,8 @@ gck_status replay_host_impl(const gck_step_record *recs, uint32_t K, const uint6
                             float *p, float *m, float *v, const uint16_t *const *glog, int threads,
                             int *threads_used, const cpu_set_t *cpus = nullptr);
 int default_threads();
+// Drain verification (replay_host.cpp): A = sum w_i, B = sum (i+1) w_i (mod 2^64) over the
+// little-endian 32-bit words of [p, p+bytes), a partial last word zero-padded.
+void checksum_host(const void *p, uint64_t bytes, uint64_t *A, uint64_t *B, int threads, const cpu_set_t *cpus);
 
 }  // namespace gck

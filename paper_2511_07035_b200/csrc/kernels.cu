@@ -21,6 +21,7 @@
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "adamw_math.cuh"
 #include "internal.h"
@@ -525,13 +526,19 @@ __global__ void __launch_bounds__((kCW + 3) * 32, 1) fused_adamw_pack_tmast_kern
     }
 }
 
+struct __align__(16) RecP {
+    RecF f;
+};
+
 __device__ __forceinline__ uint32_t part_of(const ReplayArgs &a, uint64_t e) {
     uint32_t j = 0;
     while (j + 1 < a.K && e >= a.hi[j]) ++j;
     return j;  // 0-based part index
 }
 
-__global__ void __launch_bounds__(256) replay_kernel(const ReplayArgs a) {
+// a5 GPU replay, general form: any part boundaries (per-element path where a group of 8 straddles a
+// boundary), skipped records tested per step. Used only when replay_kernel's preconditions fail.
+__global__ void __launch_bounds__(256) replay_generic_kernel(const ReplayArgs a) {
     // the K step records with their hoisted reciprocals, computed once per CTA
     __shared__ RecF srec[GCK_K_LIMIT];
     __shared__ int sskip[GCK_K_LIMIT];
@@ -578,6 +585,42 @@ __global__ void __launch_bounds__(256) replay_kernel(const ReplayArgs a) {
     }
 }
 
+// a5 GPU replay (default): brings each stale part j < K-1 (0-based) from S(t0+j) to S(T) with the
+// compacted non-skipped StepRecords j .. K-2 (ReplayPlan, built on the host). One thread owns 8
+// consecutive elements (two 16-B vectors of p, m, v), keeps them in registers across all of their
+// pending updates — the next step's gradient vector in flight while this step computes — and stores
+// them once: 24 B + 2 B per pending update per element, the algorithmic minimum. Grid-stride over
+// the groups with the part index tracked monotonically (one compare per group); every group lies in
+// one part (boundaries are multiples of 8, checked on the host). The update is adamw_group_mm:
+// the fused kernel's op sequence, one min/max guard per group and step.
+template <bool kUnitGs>
+__global__ void __launch_bounds__(256) replay_kernel(const ReplayPlan a) {
+    __shared__ RecP srec[GCK_K_LIMIT];
+    for (uint32_t q = threadIdx.x; q < a.nact; q += blockDim.x) srec[q].f = to_recf(a.rec[q]);
+    __syncthreads();
+    const uint64_t ngroups = a.n_replay >> 3;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    uint32_t j = 0;
+    for (uint64_t gi = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < ngroups; gi += stride) {
+        const uint64_t e = gi << 3;
+        while (e >= a.hi[j]) ++j;  // e only grows: amortised O(1)
+        const uint32_t q0 = a.first[j];
+        if (q0 >= a.nact) continue;  // every pending update of this part was skipped: already S(T)
+        Vec8 p = ld8(a.p + e), m = ld8(a.m + e), v = ld8(a.v + e);
+        uint4 gnext = *reinterpret_cast<const uint4 *>(a.glog[q0] + e);
+        for (uint32_t q = q0; q < a.nact; ++q) {
+            const uint4 gq = gnext;
+            if (q + 1 < a.nact) gnext = *reinterpret_cast<const uint4 *>(a.glog[q + 1] + e);
+            const uint32_t gb[8] = {gq.x & 0xFFFFu, gq.x >> 16, gq.y & 0xFFFFu, gq.y >> 16,
+                                    gq.z & 0xFFFFu, gq.z >> 16, gq.w & 0xFFFFu, gq.w >> 16};
+            adamw_group_mm<8, kUnitGs>(p.x, m.x, v.x, gb, srec[q].f);
+        }
+        st8(a.p + e, p);
+        st8(a.m + e, m);
+        st8(a.v + e, v);
+    }
+}
+
 __global__ void __launch_bounds__(512) zerocopy_drain_kernel(const ZcArgs a) {
     const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
@@ -601,6 +644,56 @@ __global__ void __launch_bounds__(512) zerocopy_drain_kernel(const ZcArgs a) {
         }
     }
 }
+
+
+// ---- drain verification (a3): checksums of the staged sections before the copy ----
+// Over the little-endian 32-bit words w_i of each section (a partial last word zero-padded):
+// A = sum w_i, B = sum (i+1) w_i, both mod 2^64 (checksum_host in replay_host.cpp computes the same
+// on the landed bytes). A single corrupted byte changes A; transposed words change B.
+__device__ __forceinline__ void sum_pair_reduce(uint64_t a, uint64_t b, unsigned long long *out) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        a += __shfl_down_sync(0xffffffffu, a, o);
+        b += __shfl_down_sync(0xffffffffu, b, o);
+    }
+    if ((threadIdx.x & 31) == 0 && (a | b)) {
+        atomicAdd(out, (unsigned long long)a);
+        atomicAdd(out + 1, (unsigned long long)b);
+    }
+}
+
+__global__ void __launch_bounds__(256) checksum_kernel(const ZcArgs a, unsigned long long *out) {
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+    for (int s = 0; s < a.count; ++s) {
+        const uint8_t *src = static_cast<const uint8_t *>(a.src[s]);
+        const uint64_t bytes = a.bytes[s];
+        uint64_t A = 0, B = 0;
+        // the 16-byte vectors of the section (src is 16-byte aligned: slot sections 256 B, live
+        // state at lo_i = a multiple of A >= 8 elements, the gradient buffer 16 B)
+        const uint64_t nv = bytes >> 4;
+        const uint4 *v4 = reinterpret_cast<const uint4 *>(src);
+        for (uint64_t v = tid; v < nv; v += stride) {
+            const uint4 q = v4[v];
+            const uint64_t sw = (uint64_t)q.x + q.y + q.z + q.w;
+            A += sw;
+            B += (4 * v + 1) * sw + (uint64_t)q.y + 2ull * q.z + 3ull * q.w;
+        }
+        // tail words (bytes % 16), the last one zero-padded
+        const uint64_t w0 = nv << 2, nw = (bytes + 3) >> 2;
+        if (tid < nw - w0) {
+            const uint64_t i = w0 + tid;
+            uint32_t w = 0;
+            for (uint64_t b = 0; b < 4 && 4 * i + b < bytes; ++b) w |= (uint32_t)src[4 * i + b] << (8 * b);
+            A += w;
+            B += (i + 1) * (uint64_t)w;
+        }
+        sum_pair_reduce(A, B, out + 2 * s);
+    }
+}
+
+// Test hook (GCK_FAULT_FLIP): XOR one byte of device memory.
+__global__ void flip_byte_kernel(uint8_t *p) { *p ^= 0x10u; }
 
 // ---- harness-only generator (gockpt_inputs.py) ----
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
@@ -774,10 +867,70 @@ int launch_fused(const FusedArgs &a, bool pack, void *stream, int num_sms) {
     return (int)cudaGetLastError();
 }
 
+// replay_kernel's preconditions: every stale part boundary a multiple of 8 elements (plans from
+// plan_parts always qualify: A % 8 == 0) and 16-byte aligned arrays; else replay_generic_kernel.
+static bool replay_plan(const ReplayArgs &a, ReplayPlan *rp, bool *unit_gs) {
+    uintptr_t al = reinterpret_cast<uintptr_t>(a.p) | reinterpret_cast<uintptr_t>(a.m) |
+                   reinterpret_cast<uintptr_t>(a.v);
+    std::memset(rp, 0, sizeof(*rp));
+    rp->p = a.p;
+    rp->m = a.m;
+    rp->v = a.v;
+    rp->n_replay = a.n_replay;
+    *unit_gs = true;
+    for (uint32_t i = 0; i + 1 < a.K; ++i) {
+        if ((a.lo[i] | a.hi[i]) & 7u) return false;
+        al |= reinterpret_cast<uintptr_t>(a.glog[i]);
+        rp->hi[i] = a.hi[i];
+        if (a.rec[i].skip) continue;
+        rp->glog[rp->nact] = a.glog[i];
+        rp->rec[rp->nact] = a.rec[i];
+        *unit_gs = *unit_gs && a.rec[i].gs == 1.0f;
+        rp->nact++;
+    }
+    {  // first[j]: the first compacted record with original index >= j (compaction keeps the order)
+        uint32_t q = 0, idx[GCK_K_LIMIT];
+        for (uint32_t i = 0, c = 0; i + 1 < a.K; ++i)
+            if (!a.rec[i].skip) idx[c++] = i;
+        for (uint32_t j = 0; j + 1 < a.K; ++j) {
+            while (q < rp->nact && idx[q] < j) ++q;
+            rp->first[j] = q;
+        }
+    }
+    const char *e = getenv("GCK_REPLAY_IMPL");
+    return (al & 15u) == 0 && !(e && e[0] == 's');
+}
+
 int launch_replay(const ReplayArgs &a, void *stream, int num_sms) {
     if (a.n_replay == 0) return 0;
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    ReplayPlan rp;
+    bool unit_gs = false;
+    if (replay_plan(a, &rp, &unit_gs)) {
+        const unsigned grid = grid_for(a.n_replay >> 3, 256, num_sms, 8);
+        if (unit_gs)
+            replay_kernel<true><<<grid, 256, 0, s>>>(rp);
+        else
+            replay_kernel<false><<<grid, 256, 0, s>>>(rp);
+        return (int)cudaGetLastError();
+    }
     const unsigned grid = grid_for((a.n_replay + 7) >> 3, 256, num_sms, 8);
-    replay_kernel<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(a);
+    replay_generic_kernel<<<grid, 256, 0, s>>>(a);
+    return (int)cudaGetLastError();
+}
+
+int launch_checksum(const ZcArgs &a, unsigned long long *d_out, void *stream, int num_sms) {
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMemsetAsync(d_out, 0, sizeof(unsigned long long) * 2 * a.count, s);
+    if (e != cudaSuccess) return (int)e;
+    uint64_t maxv = 1;
+    for (int k = 0; k < a.count; ++k) maxv = std::max<uint64_t>(maxv, a.bytes[k] >> 4);
+    checksum_kernel<<<grid_for(maxv, 256, num_sms, 4), 256, 0, s>>>(a, d_out);
+    return (int)cudaGetLastError();
+}
+
+int launch_flip_byte(void *dev_byte, void *stream) {
+    flip_byte_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<uint8_t *>(dev_byte));
     return (int)cudaGetLastError();
 }
 

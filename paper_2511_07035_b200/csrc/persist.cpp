@@ -189,6 +189,7 @@ gck_status write_checkpoint_impl(const char *path, const gck_file_header *hdr_in
     if (::ftruncate(fd, (off_t)file_bytes) != 0) {
         *err = std::string("ftruncate: ") + strerror(errno);
         ::close(fd);
+        ::unlink(tmp.c_str());
         return GCK_E_IO;
     }
     // jobs [0, 3 nblocks): state blocks (CRC -> table); then the gradient-slice blocks (-> gtable)
@@ -235,8 +236,13 @@ gck_status write_checkpoint_impl(const char *path, const gck_file_header *hdr_in
     for (auto &t : pool) t.join();
     if (failed) {
         ::close(fd);
-        *err = fault >= 0 ? "fault injected (GCK_FAULT_PERSIST)" : std::string("pwrite: ") + strerror(errno);
-        return fault >= 0 ? GCK_E_ABORTED : GCK_E_IO;
+        if (fault >= 0) {  // the injected fault models the writer dying: its partial .tmp stays behind
+            *err = "fault injected (GCK_FAULT_PERSIST)";
+            return GCK_E_ABORTED;
+        }
+        *err = std::string("pwrite: ") + strerror(errno);
+        ::unlink(tmp.c_str());  // a failed write leaves no partial file behind
+        return GCK_E_IO;
     }
     // CRC table, then the header (with its own CRC) — the last bytes of the data file
     std::vector<char> tbl(L.table_bytes, 0);
@@ -286,10 +292,12 @@ gck_status write_checkpoint_impl(const char *path, const gck_file_header *hdr_in
     ok = (::close(fd) == 0) && ok;
     if (!ok) {
         *err = std::string("write/fsync: ") + strerror(errno);
+        ::unlink(tmp.c_str());
         return GCK_E_IO;
     }
     if (::rename(tmp.c_str(), final_path.c_str()) != 0) {
         *err = std::string("rename: ") + strerror(errno);
+        ::unlink(tmp.c_str());
         return GCK_E_IO;
     }
     const std::string dir = dir_of(final_path);

@@ -56,6 +56,19 @@ __attribute__((target_clones("avx512f", "avx2", "default"))) void update_block(
     }
 }
 
+// Partial checksum of cnt 32-bit words with local indices 0..cnt-1 (see checksum_host).
+__attribute__((target_clones("avx512f", "avx2", "default"))) void sum_words(const uint32_t *__restrict w,
+                                                                         uint32_t cnt, uint64_t *a, uint64_t *b) {
+    uint64_t A = 0, B = 0;
+    for (uint32_t k = 0; k < cnt; ++k) {
+        const uint64_t x = w[k];
+        A += x;
+        B += (uint64_t)(k + 1) * x;
+    }
+    *a = A;
+    *b = B;
+}
+
 struct Task {
     uint32_t j;  // 0-based part index
     uint64_t a, b;
@@ -79,6 +92,49 @@ int default_threads() {
     }
     const unsigned h = std::thread::hardware_concurrency();
     return h ? (int)h : 1;
+}
+
+void checksum_host(const void *p, uint64_t bytes, uint64_t *A, uint64_t *B, int threads, const cpu_set_t *cpus) {
+    const uint8_t *src = static_cast<const uint8_t *>(p);
+    const uint64_t nw = bytes >> 2;
+    constexpr uint64_t kChunk = 1ull << 24;  // words per task (64 MiB)
+    const uint64_t ntask = (nw + kChunk - 1) / kChunk;
+    std::vector<uint64_t> pa(ntask, 0), pb(ntask, 0);
+    std::atomic<uint64_t> next{0};
+    auto worker = [&]() {
+        if (cpus) pthread_setaffinity_np(pthread_self(), sizeof(cpu_set_t), cpus);
+        for (;;) {
+            const uint64_t t = next.fetch_add(1, std::memory_order_relaxed);
+            if (t >= ntask) break;
+            const uint64_t w0 = t * kChunk, cnt = std::min(kChunk, nw - w0);
+            uint64_t a = 0, b = 0;
+            sum_words(reinterpret_cast<const uint32_t *>(src) + w0, (uint32_t)cnt, &a, &b);
+            pa[t] = a;
+            pb[t] = b + w0 * a;  // global weights (w0 + k + 1) = local (k + 1) + w0
+        }
+    };
+    if (threads <= 0) threads = cpus ? std::max(1, CPU_COUNT(cpus)) : default_threads();
+    threads = (int)std::min<uint64_t>((uint64_t)threads, std::max<uint64_t>(1, ntask));
+    if (threads <= 1) {
+        worker();
+    } else {
+        std::vector<std::thread> pool;
+        for (int k = 0; k < threads; ++k) pool.emplace_back(worker);
+        for (auto &th : pool) th.join();
+    }
+    uint64_t a = 0, b = 0;
+    for (uint64_t t = 0; t < ntask; ++t) {
+        a += pa[t];
+        b += pb[t];
+    }
+    if (bytes & 3) {  // partial last word, zero-padded
+        uint32_t w = 0;
+        for (uint64_t k = 0; k < (bytes & 3); ++k) w |= (uint32_t)src[4 * nw + k] << (8 * k);
+        a += w;
+        b += (nw + 1) * (uint64_t)w;
+    }
+    *A = a;
+    *B = b;
 }
 
 gck_status replay_host_impl(const gck_step_record *recs, uint32_t K, const uint64_t *lo, const uint64_t *hi,

@@ -111,6 +111,14 @@ def d2h_copy(dst_host, src_dev, nbytes=None, mode="ce", chunk_bytes=0, zc_ctas=0
                              _stream_ptr(stream)))
 
 
+def checksum(buf: np.ndarray, threads: int = 0) -> tuple[int, int]:
+    """gck_checksum over the bytes of a contiguous host array: (A, B) of the drain verification."""
+    buf = np.ascontiguousarray(buf)
+    out = (C.c_uint64 * 2)()
+    check(lib().gck_checksum(buf.ctypes.data if buf.nbytes else None, buf.nbytes, threads, out))
+    return int(out[0]), int(out[1])
+
+
 def _hdr_dict(h: L.FileHeader) -> dict:
     return {"step": h.step, "adam_t": h.adam_t, "n": h.n, "rank": h.rank, "world": h.world, "beta1": h.beta1,
             "beta2": h.beta2, "eps": h.eps, "weight_decay": h.weight_decay, "nblocks": h.nblocks,
@@ -230,7 +238,7 @@ class GoCkpt:
     def __init__(self, master, exp_avg, exp_avg_sq, param_bf16=None, *, beta1=0.9, beta2=0.999, eps=1e-8,
                  weight_decay=0.01, k_min=1, k_max=8, part_align=1024, ring_slots=2, copy_mode="ce",
                  chunk_bytes=0, zc_ctas=0, replay_threads=0, timing=True, eager_replay=True, staging="ring",
-                 numa_node=-1, replay_mode="host", ring=None, stream_buffers=0):
+                 numa_node=-1, replay_mode="host", ring=None, stream_buffers=0, verify_drain=True):
         n = master.numel()
         if exp_avg.numel() != n or exp_avg_sq.numel() != n or (param_bf16 is not None and param_bf16.numel() != n):
             raise ValueError("state tensors must have the same number of elements")
@@ -243,7 +251,7 @@ class GoCkpt:
                        replay_threads, int(timing),
                        int(eager_replay),
                        {"ring": L.STAGE_RING, "direct": L.STAGE_DIRECT, "blocking": L.STAGE_BLOCKING}[staging],
-                       numa_node, stream_buffers)
+                       numa_node, stream_buffers, int(verify_drain))
         hp = L.Hparams(beta1, beta2, eps, weight_decay)
         self.hparams = dict(beta1=beta1, beta2=beta2, eps=eps, weight_decay=weight_decay)
         # ring: an optional caller-owned uint8 CUDA tensor of >= ring_bytes_required(...) bytes

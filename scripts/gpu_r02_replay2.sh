@@ -1,0 +1,16 @@
+#!/bin/bash
+# Replay kernel v2 (min/max guard, compacted records): microbench vs the generic kernel, ncu, tests.
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" || exit 1
+out=gpurun_out/r02_replay2.jsonl; : > $out
+for impl in t s; do
+  for nk in "124439808 8" "124439808 4" "124439808 16" "842301952 8"; do
+    set -- $nk
+    r=$(GCK_REPLAY_IMPL=$impl GCK_N=$1 GCK_K=$2 timeout 300 python scripts/microbench_replay.py 2>&1 | tail -1)
+    echo "{\"impl\": \"$impl\", \"r\": $r}" >> $out
+  done
+done
+cat $out
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:replay -s 2 -c 1 \
+   -o gpurun_out/replay_v2 -f python scripts/microbench_replay.py > gpurun_out/ncu_replay_v2.log 2>&1; echo "ncu rc=$?"
+timeout 1800 python -m pytest tests/test_gpu_fastmath.py tests/test_gpu_faults.py tests/test_gpu_guard.py tests/test_gpu_parity.py tests/test_gpu_fullsize.py -q -m gpu 2>&1 | tail -15 | tee gpurun_out/r02_replay2_tests.txt

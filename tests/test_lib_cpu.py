@@ -238,3 +238,38 @@ def test_ring_bytes_required(G):
                 best = max(best, 3 * al(4 * (hi - lo)) + al(2 * (hi if i < K - 1 else 0)))
         assert G.ring_bytes_required(n, kmin, kmax, A, R) == R * best
     assert G.ring_bytes_required(0, 1, 4) == 0 and G.ring_bytes_required(100, 5, 4) == 0
+
+
+# ---------------------------------------------------------------- a3 drain verification checksum
+def _checksum_ref(b: bytes):
+    """The definition in include/gockpt.h: little-endian 32-bit words (last one zero-padded),
+    A = sum w_i, B = sum (i+1) w_i, mod 2^64 (numpy uint64 arithmetic wraps)."""
+    pad = (-len(b)) % 4
+    w = np.frombuffer(b + b"\0" * pad, dtype="<u4").astype(np.uint64)
+    idx = np.arange(1, w.size + 1, dtype=np.uint64)
+    with np.errstate(over="ignore"):
+        return int(w.sum(dtype=np.uint64)), int((w * idx).sum(dtype=np.uint64))
+
+
+@pytest.mark.parametrize("nbytes", [0, 1, 3, 4, 17, 4096, (1 << 26) + 4 * 5 + 2])
+def test_checksum_matches_definition(G, nbytes):
+    rng = np.random.default_rng(nbytes)
+    buf = rng.integers(0, 256, nbytes, dtype=np.uint8)
+    assert G.checksum(buf, threads=4) == _checksum_ref(buf.tobytes())
+    assert G.checksum(buf, threads=1) == _checksum_ref(buf.tobytes())
+
+
+def test_checksum_detects_flip_and_swap(G):
+    rng = np.random.default_rng(1)
+    buf = rng.integers(0, 256, 1 << 20, dtype=np.uint8)
+    ref = G.checksum(buf)
+    for pos in (0, 1, 12345, (1 << 20) - 1):
+        for bit in range(8):
+            b2 = buf.copy()
+            b2[pos] ^= np.uint8(1 << bit)
+            assert G.checksum(b2)[0] != ref[0]          # any single corrupted byte changes A
+    w = buf.view(np.uint32).copy()
+    w[[10, 11]] = w[[11, 10]]                            # transposed words keep A, change B
+    if w[10] != w[11]:
+        got = G.checksum(w)
+        assert got[0] == ref[0] and got[1] != ref[1]
