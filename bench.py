@@ -39,11 +39,12 @@ sys.path.insert(0, ROOT)
 
 METRIC = "per-step checkpoint stall ms & train throughput w/ ckpt; D2H GB/s vs link peak"
 WORKLOADS = {  # BASELINE.json configs
+    "flat-1m": "flat 1M-element fp32 param vector, AdamW, checkpoint split over K=4 steps, single GPU (CPU oracle runs in seconds)",
     "gpt2-small": "GPT-2 small 124M mixed-precision AdamW state, K=8 partitions, 1 B200",
     "llama2-7b": "Llama-2 7B ZeRO-1 optimizer shards across 8\u00d7B200, K=8, checkpoint every 100 steps",
     "llama2-13b": "Llama-2 13B ZeRO-1 across 2/4/8 B200, K sweep 2\u201316 (stall vs consistency-replay cost)",
 }
-DEFAULT_TOKENS = {"gpt2-small": 16 * 1024, "llama2-7b": 2 * 4096, "llama2-13b": 2048}
+DEFAULT_TOKENS = {"flat-1m": 1, "gpt2-small": 16 * 1024, "llama2-7b": 2 * 4096, "llama2-13b": 2048}
 HP = dict(beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01)
 LR = 3e-4
 T_WARM = 100  # updates already done before the bench starts (bias-correction count offset)
@@ -87,9 +88,31 @@ def parse():
                     help="host replay / persist threads (0 = the host's cores divided by the local ranks)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-sample", type=int, default=1 << 24,
-                    help="elements of the oracle sample (cpu_baseline leg, ~15 s; --impl reference uses 1/16)")
+    ap.add_argument("--cpu-sample", type=int, default=1 << 22,
+                    help="elements of the oracle sample, the same for the cpu_baseline leg and every step of "
+                         "--impl reference (~5 s of one pinned core per interval at 2^22)")
+    ap.add_argument("--spin-ms", type=float, default=1.0,
+                    help="flat-1m only: the F/B stand-in is one spin kernel of this many ms (0 = none)")
+    ap.add_argument("--rs-bucket-mb", type=int, default=512,
+                    help="N > 1 with NCCL: gradient reduce-scatter bucket size (input bytes), issued per "
+                         "bucket while the rest of the backward stand-in runs")
+    ap.add_argument("--step-log", default="",
+                    help="write one JSON line per timed training step to this path (rank-suffixed when N > 1)")
     return ap.parse_args()
+
+
+def maybe_reexec(args):
+    """`--gpus N` (N > 1) without a torchrun environment: relaunch this command under
+    torch.distributed.run with N local ranks (the driver's launch), so the N-GPU path runs as-is."""
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        import socket
+        with socket.socket() as sk:
+            sk.bind(("127.0.0.1", 0))
+            port = sk.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        sys.stdout.flush()
+        os.execv(sys.executable, cmd)
 
 
 def dist_env():
@@ -120,19 +143,27 @@ def ncu_traffic():
 
 
 # ----------------------------------------------------------------------------- oracle (CPU) timing
+_ORACLE_INPUTS = {}
+
+
 def oracle_interval_seconds(n_sample: int, K: int, interval: int, seed: int = 42) -> tuple[float, int]:
     """Time the oracle on the CPU work of one checkpoint interval over n_sample elements:
-    `interval` AdamW updates (O1 trajectory) with a K-part session (capture + O2 replay)."""
+    `interval` AdamW updates (O1 trajectory) with a K-part session (capture + O2 replay).
+    The seeded inputs are generated once per sample size (outside the timed region)."""
     import numpy as np
 
     import gockpt_inputs as gi
     import oracle
 
-    p, m, v = gi.warm_state(seed, n_sample)
-    grads = [gi.grad_bits(seed, T_WARM + s, n_sample) for s in range(1, interval + 1)]
-    recs = [oracle.make_step_record(t=T_WARM + s, lr=LR, **HP) for s in range(1, interval + 1)]
+    key = (n_sample, interval, seed)
+    if key not in _ORACLE_INPUTS:
+        _ORACLE_INPUTS.clear()
+        _ORACLE_INPUTS[key] = (gi.warm_state(seed, n_sample),
+                               [gi.grad_bits(seed, T_WARM + s, n_sample) for s in range(1, interval + 1)],
+                               [oracle.make_step_record(t=T_WARM + s, lr=LR, **HP) for s in range(1, interval + 1)])
+    (p, m, v), grads, recs = _ORACLE_INPUTS[key]
     t_start = time.perf_counter()
-    parts = oracle.make_parts(n_sample, K, 1024)
+    parts = oracle.make_parts(n_sample, K, min(1024, max(1, n_sample // K)))
     cap, glog, live = oracle.capture_session(p, m, v, grads[:K], recs[:K], parts)   # session steps 1..K
     ck = oracle.replay(cap, glog, recs[:K], parts)
     p, m, v = live
@@ -143,12 +174,71 @@ def oracle_interval_seconds(n_sample: int, K: int, interval: int, seed: int = 42
     return dt, 1
 
 
+class OneCore:
+    """Pin this process to one core while the oracle is timed ("a single Python process
+    pinned to one core"), then restore the previous affinity."""
+
+    def __enter__(self):
+        self.saved = os.sched_getaffinity(0)
+        self.core = min(self.saved)
+        os.sched_setaffinity(0, {self.core})
+        return self
+
+    def __exit__(self, *exc):
+        os.sched_setaffinity(0, self.saved)
+
+
+def oracle_baseline(args, K, steps=1, warmup=0):
+    """The oracle on one pinned core over the same bounded sample in both legs (the GPU arm's
+    cpu_baseline and every step of --impl reference): seconds per interval of the sample, and the
+    extrapolation to the full per-rank shard stated separately."""
+    n_s = min(args.cpu_sample, args.n)
+    with OneCore() as oc:
+        for _ in range(warmup):
+            oracle_interval_seconds(n_s, K, args.interval)
+        times = [oracle_interval_seconds(n_s, K, args.interval)[0] for _ in range(steps)]
+    per_sample = statistics.mean(times)
+    factor = args.n / n_s
+    per_interval = per_sample * factor
+    tps = args.interval * args.tokens / per_interval
+    return {"value": tps, "unit": unit_of(args), "cores": 1, "kind": "oracle",
+            "sample": f"{n_s} of {args.n} elements of each {args.interval}-step interval (K={K} session + O2 replay "
+                      f"+ O1 updates), on core {oc.core}; AdamW + capture + replay only, no F/B",
+            "sample_elements": n_s, "measured_s_per_interval_sample": per_sample,
+            "extrapolation_factor": factor, "extrapolated_s_per_interval": per_interval,
+            "samples_timed": len(times)}
+
+
+def unit_of(args):
+    return "steps/s" if args.model == "flat-1m" else "tokens/s"
+
+
+def config_dict(args, world):
+    """The `config` of both arms' lines (identical, so the driver can pair them)."""
+    from paper_2511_07035_b200.harness import standin_flops
+    fb = (f"spin kernel {args.spin_ms:g} ms" if args.model == "flat-1m"
+          else f"{args.model} fwd+bwd GEMM chain (cuBLAS bf16, CUDA graphs)")
+    return {"workload": args.workload, "n_per_rank": args.n, "K": args.K, "interval": args.interval,
+            "tokens_per_step_per_rank": args.tokens, "zero1_degree": args.W,
+            "fb_standin": fb,
+            "fb_tflop_per_step": 0.0 if args.model == "flat-1m" else standin_flops(args.model, args.tokens) / 1e12,
+            "copy_mode": args.copy_mode, "ring_slots": args.ring_slots, "staging": args.staging,
+            "scheme": args.scheme, "replay_mode": args.replay_mode,
+            "dist_backend": args.dist_backend if world > 1 else None,
+            "rs_bucket_mb": args.rs_bucket_mb if world > 1 and args.dist_backend == "nccl" else None,
+            "parallelism": f"zero1-dp{world}",
+            "l2": f"inputs larger than L2 ({12 * args.n / 1e9:.2f} GB fp32 state + {2 * args.n / 1e9:.2f} GB "
+                  f"gradient per step per rank)" if args.n * 14 > 126e6 else
+                  "state smaller than L2: the checkpoint-free and session steps see the same cache state",
+            "step": "one checkpoint interval (I training steps, one K-part session, finalize)"}
+
+
 def resolve(args):
     """Per-rank shard size and tokens from --model / --shard-of (ZeRO-1)."""
-    from paper_2511_07035_b200.harness import MODELS, zero1_shard
+    from paper_2511_07035_b200.harness import FLAT_1M, MODELS, zero1_shard
     world, rank, _ = dist_env()
     W = args.shard_of or world
-    N = MODELS[args.model][0]
+    N = FLAT_1M if args.model == "flat-1m" else MODELS[args.model][0]
     if not args.n:
         args.n = N if W == 1 else zero1_shard(N, W, min(rank, W - 1), 512)[1]
     if not args.tokens:
@@ -162,36 +252,31 @@ def run_reference(args):
     world, rank, _ = dist_env()
     if world > 1 and rank != 0:
         return
-    n_s = min(args.cpu_sample // 16, args.n)
-    for _ in range(args.warmup):
-        oracle_interval_seconds(min(n_s, 1 << 16), args.K, args.interval)
-    times = []
     t0 = time.perf_counter()
-    for _ in range(args.steps):
-        dt, _ = oracle_interval_seconds(n_s, args.K, args.interval)
-        times.append(dt * args.n / n_s)   # extrapolated to the full per-rank shard
-    wall = time.perf_counter() - t0
-    per_interval = statistics.mean(times)
-    value = args.interval * args.tokens / per_interval
-    cores = 1
+    cpu = oracle_baseline(args, args.K if args.K else 8, steps=args.steps, warmup=args.warmup)
+    cpu["wall_s"] = time.perf_counter() - t0
+    value = cpu["value"]
     line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_interval * 1e3, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": args.workload, "n_per_rank": args.n, "K": args.K, "interval": args.interval,
-                   "tokens_per_step": args.tokens, "zero1_degree": args.W},
-        "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cores, "kind": "oracle",
-                         "sample": f"{n_s} of {args.n} elements per interval, time x{args.n / n_s:.1f}; "
-                                   f"the oracle's AdamW + capture + replay only (no F/B)",
-                         "wall_s": wall},
-        "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "impl": "reference", "metric": METRIC, "value": value, "unit": unit_of(args), "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": cpu["extrapolated_s_per_interval"] * 1e3,
+        "ms_per_step_note": "extrapolated: measured_s_per_interval_sample x extrapolation_factor "
+                            "(cpu_baseline); the measured wall time of this run is cpu_baseline.wall_s",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": config_dict(args, world),
+        "cpu_baseline": cpu,
+        "e2e": {"value": value, "unit": unit_of(args), "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
 # ----------------------------------------------------------------------------- the GPU arm
 def main():
-    args = resolve(parse())
+    args = parse()
+    maybe_reexec(args)
+    args = resolve(args)
+    world, _, _ = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} (launch N ranks for --gpus N)")
     if args.impl == "reference":
         return run_reference(args)
     assert args.warmup >= 3, "W >= 3 warm-up steps"
@@ -201,7 +286,8 @@ def main():
 
     import paper_2511_07035_b200 as G
     from paper_2511_07035_b200 import build as gbuild
-    from paper_2511_07035_b200.harness import ClockSampler, TransformerGemmStandIn, max_over_ranks, all_ranks_ok
+    from paper_2511_07035_b200.harness import (ClockSampler, SpinStandIn, TransformerGemmStandIn, all_ranks_ok,
+                                               max_over_ranks, rs_buckets)
 
     world, rank, local = dist_env()
     if not torch.cuda.is_available():
@@ -211,6 +297,9 @@ def main():
     coll = world > 1 and args.dist_backend == "nccl"   # the harness's NCCL reduce-scatter / all-gather
     if world > 1:
         if args.dist_backend == "nccl":
+            # NCCL's INFO lines (transport, NVLS) stay on, on stderr (stdout carries the JSON line)
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group("gloo")
@@ -235,8 +324,17 @@ def main():
     if coll:
         full_grad = torch.empty(n * world, dtype=torch.bfloat16, device=dev)
         full_param = torch.empty(n * world, dtype=torch.bfloat16, device=dev)
-    fb = TransformerGemmStandIn(args.model, tokens=T, device=dev)
-    fb.capture()
+    if args.model == "flat-1m":
+        fb = SpinStandIn(args.spin_ms, device=dev)
+    else:
+        fb = TransformerGemmStandIn(args.model, tokens=T, device=dev)
+    # N > 1 (NCCL): the ZeRO-1 gradient reduce-scatter runs per bucket (512 MB buckets)
+    # as soon as the backward part that "produced" the bucket is done, overlapping the rest of it
+    buckets = rs_buckets(n, world, args.rs_bucket_mb << 20) if coll else []
+    bwd_parts = max(1, min(8, len(buckets)))
+    fb.capture(bwd_parts)
+    part_buckets = [buckets[k * len(buckets) // bwd_parts:(k + 1) * len(buckets) // bwd_parts]
+                    for k in range(bwd_parts)]
     auto_k = K == 0
     ctx = G.GoCkpt(master, exp_avg, exp_avg_sq, param, **HP, k_min=1 if auto_k else K, k_max=32 if auto_k else K,
                    part_align=1024,
@@ -249,24 +347,38 @@ def main():
         side = torch.cuda.Stream()
     state = {"step": 0, "gen": 0, "K": K if not auto_k else 32, "auto": auto_k}
 
-    # ---- host-link peak: best-of-5 1 GiB D2H into pinned memory, measured in this run
+    # ---- host-link peak: best-of-5 1 GiB D2H into pinned memory, measured in this run — rank 0 alone
+    #      (the others wait at a barrier), then all ranks at once (the rate the sessions' drains share)
     link = torch.empty(1 << 30, dtype=torch.uint8, device=dev)
     link_h = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
-    best = 1e9
-    for _ in range(5):
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record()
-        link_h.copy_(link, non_blocking=True)
-        b.record()
-        b.synchronize()
-        best = min(best, a.elapsed_time(b))
-    link_peak = (1 << 30) / best / 1e6
+
+    def d2h_peak():
+        best = 1e9
+        for _ in range(5):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            link_h.copy_(link, non_blocking=True)
+            b.record()
+            b.synchronize()
+            best = min(best, a.elapsed_time(b))
+        return (1 << 30) / best / 1e6
+
+    if world > 1:
+        dist.barrier()
+    link_alone = d2h_peak() if rank == 0 else 0.0
+    if world > 1:
+        dist.barrier()
+        link_peak = d2h_peak()          # this rank, all ranks copying concurrently
+        dist.barrier()
+    else:
+        link_peak = link_alone
     del link, link_h
 
     result_host = []
     e2e_io = {}
     plain_bytes = 28 * n
-    kern = {"plain_ms": [], "plain_bytes": 0, "sess_ms0": 0.0, "sess_n0": 0, "sess_bytes": 0}
+    kern = {"plain_ms": [], "plain_step": [], "plain_bytes": 0, "sess_ms0": 0.0, "sess_n0": 0, "sess_bytes": 0}
+    sess_log = []   # per timed session: (first training step, gck_get_session_steps entries)
 
     def train_step(part, h_grad=None, time_kernel=False, step_events=None, snapshot=False):
         state["step"] += 1
@@ -292,15 +404,27 @@ def main():
             with torch.cuda.stream(loader):
                 g_in.copy_(h_grad[s % len(h_grad)], non_blocking=True)
             e2e_io["loaded"].record(loader)
-        fb()                                                           # F/B stand-in
+        torch.cuda.nvtx.range_push(f"step {s} F/B")
+        fb.forward()                                                   # F/B stand-in
+        works = []
+        for k in range(fb.bwd_parts):
+            fb.backward(k)
+            if h_grad is None and coll:
+                # the buckets this backward part completed (harness generator = the local gradient,
+                # bucket-major layout [bucket][rank][count]) go out while the rest of the backward runs
+                for off, cnt in part_buckets[k]:
+                    src = full_grad[world * off:world * (off + cnt)]
+                    G.h_generate(G.GEN_GRAD, src.view(torch.int16), seed, s, world * off, 1, 4)
+                    state["gen"] += 1
+                    works.append(dist.reduce_scatter_tensor(grad[off:off + cnt].view(torch.bfloat16), src,
+                                                            async_op=True))
+        torch.cuda.nvtx.range_pop()
         ctx.grad_fence(stream)   # direct staging: the last gradient slice is out before we overwrite
         if h_grad is not None:
             stream.wait_event(e2e_io["loaded"])
         elif coll:
-            # backward's full local gradient (harness generator), then the ZeRO-1 reduce-scatter
-            G.h_generate(G.GEN_GRAD, full_grad.view(torch.int16), seed, s, 0, 1, 4)
-            state["gen"] += 1
-            dist.reduce_scatter_tensor(grad.view(torch.bfloat16), full_grad)
+            for w in works:      # the update consumes the reduced shard
+                w.wait()
         else:
             G.h_generate(G.GEN_GRAD, grad, seed, s, rank * n, 1, 4)    # backward's gradient (harness)
             state["gen"] += 1
@@ -314,6 +438,7 @@ def main():
         if a is not None:
             b.record(stream)
             kern["plain_ms"].append((a, b))
+            kern["plain_step"].append(s)
         if h_grad is not None:   # e2e: the step's result (first 8 bytes of the updated bf16 params) to host
             result_host[s % 2].copy_(param[:4], non_blocking=True)
         if coll:
@@ -347,6 +472,8 @@ def main():
         if ckpt:
             ck = ctx.finalize()
             assert ck.step == state["step"] - I + state["K"] - 1
+            if state.get("log_sessions"):
+                sess_log.append((state["step"] - I + 1, ctx.session_steps()))
             ctx.release()
             assert all_ranks_ok(True)
 
@@ -384,11 +511,14 @@ def main():
     gen0 = state["gen"]
     step_ev = []
     clocks = ClockSampler(local).start()
+    first_timed_step = state["step"] + 1
+    state["log_sessions"] = True
     t_ck = timed(args.steps, ckpt=True, time_kernel=True, step_events=step_ev)
+    state["log_sessions"] = False
     clk = clocks.stop()
     st1 = ctx.stats()
     gpu_launches = (st1["gpu_launches"] - st0["gpu_launches"]) + (state["gen"] - gen0)
-    tokens_total = args.steps * I * T * world
+    tokens_total = args.steps * I * T * world   # flat-1m: T = 1, the value is training steps/s
     value = tokens_total / t_ck
     # step times inside the timed region (event deltas); session steps are the first K of each interval
     step_ms = [step_ev[k].elapsed_time(step_ev[k + 1]) for k in range(len(step_ev) - 1)]
@@ -396,7 +526,8 @@ def main():
     sess_ms = [t for k, t in enumerate(step_ms) if (k % I) < K_aff]
     plain_ms_steps = [t for k, t in enumerate(step_ms) if (k % I) >= K_aff]
     kern_plain = [a.elapsed_time(b) for a, b in kern["plain_ms"]]
-    kern["plain_ms"] = []
+    plain_kernel_of_step = dict(zip(kern["plain_step"], kern_plain))
+    kern["plain_ms"], kern["plain_step"] = [], []
     sess_kernel_ms = st1["kernel_ms_total"] - st0["kernel_ms_total"]
     sess_launches = st1["kernel_launches_timed"] - st0["kernel_launches_timed"]
     # roofline of the dominant launch kind (plain steps: 28 B/element, I-K of every I launches)
@@ -437,7 +568,7 @@ def main():
         torch.cuda.synchronize()
         interval(ckpt=True, h_grad=h_grads)   # warm the path
         t_e2e = timed(max(1, args.steps), ckpt=True, h_grad=h_grads)
-        e2e = {"value": max(1, args.steps) * I * T * world / t_e2e, "unit": "tokens/s",
+        e2e = {"value": max(1, args.steps) * I * T * world / t_e2e, "unit": unit_of(args),
                "h2d_bytes_per_step": 2 * n, "d2h_bytes_per_step": 8 + session_bytes / I,
                "note": "the reduced bf16 gradient shard arrives by H2D from pinned host memory every step "
                        "(prefetched on a copy stream into one of two device buffers while the step's F/B runs, "
@@ -445,15 +576,10 @@ def main():
                        "step reads 8 bytes of the updated params back (the step's result), and the "
                        "checkpoint the library drains is the session's result (D2H)"}
 
-    # ---- oracle on host cores (rank 0, N=1 only)
+    # ---- oracle on one pinned host core (rank 0, N=1 only), the same sample as --impl reference
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        n_s = min(args.cpu_sample, n)
-        dt, _ = oracle_interval_seconds(n_s, K, I)
-        per_interval = dt * n / n_s
-        cpu = {"value": I * T / per_interval, "unit": "tokens/s", "cores": 1, "kind": "oracle",
-               "sample": f"{n_s} of {n} elements of one {I}-step interval (K={K} session + replay), "
-                         f"{dt:.1f} s measured, time scaled x{n / n_s:.1f}; AdamW + capture + replay only, no F/B"}
+        cpu = oracle_baseline(args, K)
 
     sess_stall_delta = [max(0.0, t - free_med) for t in sess_ms]
     # bootstrap 95% CI of the mean delta per session step, resampling whole sessions
@@ -462,13 +588,39 @@ def main():
     boot = [float(np.mean(rng.choice(per_sess, len(per_sess)))) for _ in range(2000)]
     delta_ci95 = [float(np.percentile(boot, 2.5)), float(np.percentile(boot, 97.5))]
     ctx_stats_final = ctx.stats()
+    d2h_gbs = d2h_bytes / (d2h_ms / 1e3) / 1e9 if d2h_ms > 0 else None
+    mine = {"rank": rank, "wait_ms_per_session_step": stall_wait_ms / (args.steps * K),
+            "delta_ms_per_session_step_mean": statistics.mean(sess_stall_delta),
+            "delta_frac_of_step": statistics.mean(sess_stall_delta) / free_med,
+            "d2h_gbs": d2h_gbs, "link_peak_concurrent_gbs": link_peak, "ckpt_free_step_ms_median": free_med}
+    per_rank = [mine]
+    if world > 1:
+        per_rank = [None] * world
+        dist.all_gather_object(per_rank, mine)
+    # ---- per-step log of the timed region (SURVEY §5 metrics): one JSON line per training step
+    if args.step_log:
+        recs = {}
+        for s0, steps in sess_log:
+            for e in steps:
+                recs[s0 + e["part"] - 1] = e
+        path = args.step_log if world == 1 else f"{args.step_log}.rank{rank}"
+        with open(path, "w") as fh:
+            for k, t in enumerate(step_ms):
+                st_idx = first_timed_step + k
+                e = recs.get(st_idx)
+                fh.write(json.dumps({
+                    "step": st_idx, "interval": k // I, "part": e["part"] if e else 0, "rank": rank,
+                    "t_step_ms": t, "stall_ms": t - free_med, "wait_ms": e["wait_ms"] if e else 0.0,
+                    "fused_ms": e["kernel_ms"] if e else plain_kernel_of_step.get(st_idx),
+                    "d2h_bytes": e["d2h_bytes"] if e else 0, "d2h_ms": e["d2h_ms"] if e else 0.0,
+                    "slot": (None if e["slot"] == 0xFFFFFFFF else e["slot"]) if e else None}) + "\n")
     # NEXT-4: the analytic model's K for this step time and link (smallest K whose largest per-step
     # transfer fits in one step), next to the K this run used
     k_rec, vmax_rec = G.recommend_k(n, link_peak, free_med / 1e3, 1.0, 64)
     line = {
         "metric": METRIC,
         "value": value,
-        "unit": "tokens/s",
+        "unit": unit_of(args),
         "n_gpus": world,
         "steps": args.steps,
         "warmup": args.warmup,
@@ -478,16 +630,7 @@ def main():
         "vs_baseline": None,
         "dtype": "f32",
         "data": "synthetic",
-        "config": {"workload": args.workload, "n_per_rank": n, "K": K, "interval": I, "tokens_per_step_per_rank": T,
-                   "zero1_degree": args.W,
-                   "fb_standin": f"{args.model} fwd+bwd GEMM chain (cuBLAS bf16, CUDA graph)",
-                   "fb_tflop_per_step": fb.flops / 1e12, "copy_mode": args.copy_mode,
-                   "ring_slots": args.ring_slots, "staging": args.staging, "scheme": args.scheme,
-                   "replay_mode": args.replay_mode, "dist_backend": args.dist_backend if world > 1 else None,
-                   "parallelism": f"zero1-dp{world}",
-                   "l2": f"inputs larger than L2 ({12 * n / 1e9:.2f} GB fp32 state + {2 * n / 1e9:.2f} GB gradient "
-                         f"per step per rank)",
-                   "step": "one checkpoint interval (I training steps, one K-part session, finalize)"},
+        "config": dict(config_dict(args, world), K=K),
         "stall": {"wait_ms_per_session_step": stall_wait_ms / (args.steps * K),
                   "wait_ms_max": st1["stall_ms_max"],
                   "session_step_ms_median": statistics.median(sess_ms),
@@ -507,13 +650,23 @@ def main():
                                 "plain_step_ms_median with ckpt_free_step_ms_median); *_vs_plain_steps_same_intervals "
                                 "compares them with the plain steps of the same timed intervals",
                   "amortized_frac": (t_ck - t_free) / t_free},
-        "ckpt_free": {"value": value_free, "unit": "tokens/s", "throughput_ratio": value / value_free,
+        "per_rank": {"ranks": per_rank,
+                     "max_wait_ms_per_session_step": max(r["wait_ms_per_session_step"] for r in per_rank),
+                     "max_delta_ms_per_session_step_mean": max(r["delta_ms_per_session_step_mean"] for r in per_rank),
+                     "max_delta_frac_of_step": max(r["delta_frac_of_step"] for r in per_rank),
+                     "min_d2h_gbs": min((r["d2h_gbs"] or 0.0) for r in per_rank),
+                     "max_d2h_gbs": max((r["d2h_gbs"] or 0.0) for r in per_rank),
+                     "note": "SURVEY §8(d) M1 target: max over ranks of the per-session-step stall < 5% of the "
+                             "checkpoint-free step"},
+        "ckpt_free": {"value": value_free, "unit": unit_of(args), "throughput_ratio": value / value_free,
                       "how": "checkpoint-free intervals measured before and after the timed region, same run"},
-        "d2h": {"gbs": d2h_bytes / (d2h_ms / 1e3) / 1e9 if d2h_ms > 0 else None,
-                "link_peak_gbs": link_peak, "frac": (d2h_bytes / (d2h_ms / 1e3) / 1e9) / link_peak if d2h_ms else None,
-                "frac_of_nominal_pcie5_x16": (d2h_bytes / (d2h_ms / 1e3) / 1e9) / 64.0 if d2h_ms else None,
+        "d2h": {"gbs": d2h_gbs,
+                "link_peak_gbs": link_peak, "frac": d2h_gbs / link_peak if d2h_gbs else None,
+                "link_peak_alone_gbs": link_alone, "link_peak_concurrent_gbs": link_peak,
+                "frac_of_nominal_pcie5_x16": d2h_gbs / 64.0 if d2h_gbs else None,
                 "bytes_per_session": session_bytes, "link_peak_how": "best of 5 x 1 GiB cudaMemcpyAsync D2H "
-                "into pinned memory, this run"},
+                "into pinned memory, this run: rank 0 alone (the others at a barrier), then every rank at once "
+                "(link_peak_gbs = this rank's concurrent figure; the two coincide at N = 1)"},
         "model": {"recommended_K": k_rec, "v_max_bytes_at_recommended_K": vmax_rec, "K_used": K,
                   "K_automatic": auto_k, "auto_step_ms": ctx_stats_final.get("auto_step_ms"),
                   "auto_link_gbs": ctx_stats_final.get("auto_link_gbs"),

@@ -211,6 +211,18 @@ typedef struct {
                                       drain verification (cfg.verify_drain) before the replay */
 } gck_stats;
 
+/* One session step of the last finalized session (gck_get_session_steps): the per-step log behind
+ * the stall metric (a4) and the drain rate (a3). Times need cfg.timing (else 0). */
+typedef struct {
+    uint32_t part;        /* session step i (1..K) */
+    uint32_t slot;        /* ring slot it packed into ((i-1) mod R); UINT32_MAX for direct staging */
+    float wait_ms;        /* the slot-reuse (direct: state-copy) wait on the compute stream before the update */
+    float kernel_ms;      /* the fused AdamW + pack kernel */
+    float d2h_ms;         /* this step's D2H copies on the drain stream (copy-engine busy time) */
+    uint32_t _pad;
+    uint64_t d2h_bytes;   /* bytes this step drained: 12 |P_i| + 2 hi_i (i < K) */
+} gck_session_step;
+
 /* ---- context lifecycle -------------------------------------------------- */
 
 /* HBM bytes the ring needs for (n, K in [k_min, k_max], A, R slots): R x the largest
@@ -298,6 +310,10 @@ gck_status gck_sync_snapshot(gck_ctx *ctx, void *stream, float *h_master, float 
 gck_status gck_replay_gpu(gck_ctx *ctx, void *stream, float *d_master, float *d_m, float *d_v, uint16_t *d_glog);
 
 gck_status gck_get_stats(const gck_ctx *ctx, gck_stats *out);
+
+/* Per-step log of the last finalized session: writes min(K, cap) entries, *count = K (0 before the
+ * first finalized session). Host-only. Errors: INVALID (NULL ctx/count, or out NULL with cap > 0). */
+gck_status gck_get_session_steps(const gck_ctx *ctx, gck_session_step *out, uint32_t cap, uint32_t *count);
 const char *gck_last_error(const gck_ctx *ctx);
 
 /* ---- stateless building blocks (used by the context; exported for tests) */

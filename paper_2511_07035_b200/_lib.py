@@ -86,6 +86,14 @@ class Stats(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_ if not k.startswith("_")}
 
 
+class SessionStep(C.Structure):
+    _fields_ = [("part", C.c_uint32), ("slot", C.c_uint32), ("wait_ms", C.c_float), ("kernel_ms", C.c_float),
+                ("d2h_ms", C.c_float), ("_pad", C.c_uint32), ("d2h_bytes", C.c_uint64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_ if not k.startswith("_")}
+
+
 class FileHeader(C.Structure):
     _fields_ = [("magic", C.c_char * 8), ("version", C.c_uint32), ("header_bytes", C.c_uint32),
                 ("step", C.c_uint64), ("adam_t", C.c_uint64), ("n", C.c_uint64), ("rank", C.c_uint32),
@@ -128,6 +136,7 @@ SIGNATURES = {
     "gck_sync_snapshot": (C.c_int, [P, P, P, P, P]),
     "gck_replay_gpu": (C.c_int, [P, P, P, P, P, P]),
     "gck_get_stats": (C.c_int, [P, C.POINTER(Stats)]),
+    "gck_get_session_steps": (C.c_int, [P, C.POINTER(SessionStep), C.c_uint32, C.POINTER(C.c_uint32)]),
     "gck_last_error": (C.c_char_p, [P]),
     "gck_make_step_record": (C.c_int, [C.POINTER(Hparams), C.c_uint64, C.c_double, C.c_double, C.c_int32,
                                        C.POINTER(StepRecord)]),

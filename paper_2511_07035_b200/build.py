@@ -73,7 +73,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     _run(gxx + ["-c", os.path.join(CSRC, "model.cpp"), "-o", objs["model"]], log)
     tmp = LIB + ".tmp"
     _run([nvcc, *ARCH, "-shared", "-cudart", "static", "-o", tmp, objs["kernels"], objs["runtime"],
-          objs["replay_host"], objs["persist"], objs["model"], "-Xcompiler", "-fPIC", "-lpthread", "-lz"], log)
+          objs["replay_host"], objs["persist"], objs["model"], "-Xcompiler", "-fPIC", "-lpthread", "-lz", "-ldl"], log)
     os.replace(tmp, LIB)
     with open(os.path.join(BUILD, "build.log"), "w") as fh:
         fh.write("\n".join(log))

@@ -33,6 +33,7 @@
 #include <vector>
 
 #include "internal.h"
+#include "nvtx3/nvToolsExt.h"
 
 using gck::FusedArgs;
 using gck::ReplayArgs;
@@ -41,6 +42,18 @@ using gck::ZcArgs;
 namespace {
 
 thread_local std::string g_tls_error;
+
+// NVTX ranges on the host timeline (nsys -t cuda,nvtx,osrt shows them next to the kernels and the
+// D2H copies); header-only NVTX v3, a no-op unless a profiler injects itself.
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    NvtxRange(const char *what, uint32_t i) {
+        char b[64];
+        snprintf(b, sizeof(b), "%s %u", what, i);
+        nvtxRangePushA(b);
+    }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 constexpr uint64_t kAlign = 256;
 inline uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
@@ -290,6 +303,8 @@ struct gck_ctx {
     double pow1 = 1.0, pow2 = 1.0;
 
     gck_stats stats{};
+    gck_session_step step_log[GCK_K_LIMIT]{};  // the last finalized session, per step
+    uint64_t step_bytes[GCK_K_LIMIT]{};        // D2H bytes enqueued per session step (this session)
 
     gck_status fail(gck_status st, const std::string &msg) {
         last_error = msg;
@@ -354,6 +369,7 @@ struct gck_ctx {
     // 1..i+1 are then all at S(t0+i+1). After slice K-2, parts 1..K-1 are at S(T). Each element of
     // part j gets updates t0+j .. T in ascending order — the batch replay's op sequence.
     void run_stream() {
+        NvtxRange nv("streaming replay worker");
         const auto t_start = std::chrono::steady_clock::now();
         gck_status st = GCK_OK;
         double comp = 0;
@@ -374,6 +390,7 @@ struct gck_ctx {
                 }
                 const auto r0 = std::chrono::steady_clock::now();
                 if ((st = check_step(i + 1)) != GCK_OK || (st = verify_step(i + 1)) != GCK_OK) break;
+                NvtxRange nvs("stream: apply slice", i + 1);
                 const gck_step_record r2[2] = {recs[i], recs[i]};
                 const uint64_t lo2[2] = {0, hi[i]}, hi2[2] = {hi[i], cfg.n};
                 const uint16_t *g2[2] = {glog[i], nullptr};
@@ -514,6 +531,7 @@ struct gck_ctx {
 
     // Runs on the worker thread (eager) or inside finalize.
     void run_replay() {
+        NvtxRange nv("replay worker (verify + replay)");
         const auto t_start = std::chrono::steady_clock::now();
         gck_status st = GCK_OK;
         {
@@ -564,20 +582,35 @@ struct gck_ctx {
 
     void collect_session_timing() {
         double stall = 0, d2h_ms = 0, kern = 0;
+        std::memset(step_log, 0, sizeof(step_log));
+        for (uint32_t i = 0; i < K; ++i) {
+            gck_session_step &sl = step_log[i];
+            sl.part = i + 1;
+            sl.slot = direct ? UINT32_MAX : i % R;
+            sl.d2h_bytes = step_bytes[i];
+        }
         if (cfg.timing) {
             for (uint32_t i = 0; i < K; ++i) {
                 float a = 0, b = 0, c = 0;
                 if (cudaEventElapsedTime(&a, ev_w0[i], ev_w1[i]) == cudaSuccess) {
                     stall += a;
+                    step_log[i].wait_ms = a;
                     if (a > stats.stall_ms_max) stats.stall_ms_max = a;
                 }
                 if (cudaEventElapsedTime(&b, ev_w1[i], ev_k1[i]) == cudaSuccess) {
                     kern += b;
+                    step_log[i].kernel_ms = b;
                     stats.kernel_launches_timed++;
                 }
-                if (cudaEventElapsedTime(&c, ev_d0[i], ev_d1[i]) == cudaSuccess) d2h_ms += c;
+                if (cudaEventElapsedTime(&c, ev_d0[i], ev_d1[i]) == cudaSuccess) {
+                    d2h_ms += c;
+                    step_log[i].d2h_ms = c;
+                }
                 float gms = 0;
-                if (direct && i + 1 < K && cudaEventElapsedTime(&gms, ev_g0[i], ev_g1[i]) == cudaSuccess) d2h_ms += gms;
+                if (direct && i + 1 < K && cudaEventElapsedTime(&gms, ev_g0[i], ev_g1[i]) == cudaSuccess) {
+                    d2h_ms += gms;
+                    step_log[i].d2h_ms += gms;
+                }
             }
         }
         stats.stall_ms_total += stall;
@@ -959,6 +992,7 @@ static cudaError_t enqueue_state_copy(gck_ctx *c, uint32_t i) {
         if (c->cfg.timing) cudaEventRecord(c->ev_d1[i - 1], c->d2h);
         c->stats.d2h_bytes += 3 * pe * 4;
         c->stats.last_session_d2h_bytes += 3 * pe * 4;
+        c->step_bytes[i - 1] += 3 * pe * 4;
         c->state_mask |= 1ull << (i - 1);
     } else if (c->cfg.timing) {
         cudaEventRecord(c->ev_d0[i - 1], c->d2h);
@@ -1000,6 +1034,7 @@ static uint32_t auto_k(gck_ctx *c) {
 
 gck_status gck_begin_checkpoint(gck_ctx *c, uint64_t t0, uint32_t K) {
     if (!c) return set_tls(GCK_E_INVALID, "null ctx");
+    NvtxRange nv("gck_begin_checkpoint K", K);
     if (c->poisoned) return c->fail(GCK_E_CUDA, "context poisoned by an earlier CUDA failure");
     if (c->state != State::IDLE && c->state != State::ABORTED)
         return c->fail(GCK_E_PROTOCOL, "begin_checkpoint while a session or an unreleased checkpoint is live");
@@ -1028,6 +1063,7 @@ gck_status gck_begin_checkpoint(gck_ctx *c, uint64_t t0, uint32_t K) {
     if (off > c->glog_elems_cap) return c->fail(GCK_E_INVALID, "gradient log capacity exceeded");
     c->stats.last_session_d2h_bytes = 0;
     c->state_mask = c->grad_mask = 0;
+    std::memset(c->step_bytes, 0, sizeof(c->step_bytes));
     c->worker_error.clear();
     c->K = K;  // the drain/verify paths below read K
     {  // test hooks (session step numbers, 1-based): a slice that never drains / one corrupted landed byte
@@ -1120,6 +1156,7 @@ static gck_status enqueue_checksum(gck_ctx *c, uint32_t i, const void *const *sr
 
 static gck_status enqueue_drain(gck_ctx *c, uint32_t i, const SlotLayout &L, char *slot) {
     // slot -> host ckpt arrays at offset lo_i, gradient -> glog[i]
+    NvtxRange nv("drain enqueue", i);
     if (drain_fault(i)) return GCK_E_ABORTED;
     if (c->fault_drop == i) return GCK_OK;  // test hook: the slice silently never drains
     const uint64_t lo = c->lo[i - 1], pe = c->hi[i - 1] - lo;
@@ -1136,6 +1173,7 @@ static gck_status enqueue_drain(gck_ctx *c, uint32_t i, const SlotLayout &L, cha
     const uint64_t tot = bytes[0] + bytes[1] + bytes[2] + bytes[3];
     c->stats.d2h_bytes += tot;
     c->stats.last_session_d2h_bytes += tot;
+    c->step_bytes[i - 1] += tot;
     c->state_mask |= 1ull << (i - 1);
     if (ghi) c->grad_mask |= 1ull << (i - 1);
     return GCK_OK;
@@ -1200,6 +1238,7 @@ static gck_status submit_direct(gck_ctx *c, uint32_t i, const gck_step_args *a, 
             c->stats.gpu_launches += (uint64_t)r;
             c->stats.d2h_bytes += ghi * 2;
             c->stats.last_session_d2h_bytes += ghi * 2;
+            c->step_bytes[i - 1] += ghi * 2;
             c->grad_mask |= 1ull << (i - 1);
         }
     }
@@ -1248,6 +1287,7 @@ gck_status gck_grad_fence(gck_ctx *c, void *stream) {
 
 gck_status gck_submit(gck_ctx *c, uint32_t part, const gck_step_args *a, void *stream) {
     if (!c) return set_tls(GCK_E_INVALID, "null ctx");
+    NvtxRange nv("gck_submit part", part);
     if (!a || !a->grad_bf16) return c->fail(GCK_E_INVALID, "null step args or gradient");
     if (!aligned16(a->grad_bf16)) return c->fail(GCK_E_INVALID, "gradient must be 16-byte aligned");
     if (c->poisoned) return c->fail(GCK_E_CUDA, "context poisoned by an earlier CUDA failure");
@@ -1400,6 +1440,7 @@ gck_status gck_get_staged(gck_ctx *c, gck_staged *out) {
 
 static gck_status finalize_impl(gck_ctx *c, gck_checkpoint *out, bool block) {
     if (!c || !out) return set_tls(GCK_E_INVALID, "null argument");
+    NvtxRange nv(block ? "gck_finalize" : "gck_finalize_poll");
     if (c->state == State::ABORTED) return c->fail(c->abort_status, c->last_error);
     if (c->state == State::ACTIVE || c->state == State::IDLE)
         return c->fail(GCK_E_PROTOCOL, "finalize before part K was submitted");
@@ -1627,6 +1668,7 @@ gck_status gck_persist_begin(gck_ctx *c, const char *path, uint32_t rank, uint32
     // replay-on-restore: the captured parts go out with the gradient log and the StepRecords
     const bool deferred = c->cfg.replay_mode == GCK_REPLAY_DEFERRED && c->K > 1;
     c->persist_worker = std::thread([c, h, p, meta, deferred]() {
+        NvtxRange nv("persist");
         if (c->numa >= 0) pthread_setaffinity_np(pthread_self(), sizeof(cpu_set_t), &c->numa_cpus);
         const float *sec[3] = {c->h_master, c->h_m, c->h_v};
         gck::ReplayLog log;
@@ -1662,6 +1704,7 @@ gck_status gck_persist_wait(gck_ctx *c, gck_persist_stats *out) {
 
 gck_status gck_restore(gck_ctx *c, const char *path, void *stream, gck_file_header *out) {
     if (!c || !path) return set_tls(GCK_E_INVALID, "null argument");
+    NvtxRange nv("gck_restore");
     if (c->state != State::IDLE) return c->fail(GCK_E_PROTOCOL, "restore while a session or checkpoint is live");
     c->join_persist();
     c->join_worker();
@@ -1732,6 +1775,14 @@ gck_status gck_restore(gck_ctx *c, const char *path, void *stream, gck_file_head
 gck_status gck_checksum(const void *host, uint64_t bytes, int32_t threads, uint64_t *out_ab) {
     if (!out_ab || (!host && bytes)) return set_tls(GCK_E_INVALID, "null argument");
     gck::checksum_host(host, bytes, &out_ab[0], &out_ab[1], threads, nullptr);
+    return GCK_OK;
+}
+
+gck_status gck_get_session_steps(const gck_ctx *c, gck_session_step *out, uint32_t cap, uint32_t *count) {
+    if (!c || !count || (cap && !out)) return set_tls(GCK_E_INVALID, "null argument");
+    const uint32_t k = (c->stats.sessions && c->step_log[0].part) ? c->K : 0;
+    *count = k;
+    for (uint32_t i = 0; i < k && i < cap; ++i) out[i] = c->step_log[i];
     return GCK_OK;
 }
 

@@ -330,6 +330,13 @@ class GoCkpt:
         check(lib().gck_restore(self._ctx, path.encode(), _stream_ptr(stream), C.byref(h)), self._ctx)
         return _hdr_dict(h)
 
+    def session_steps(self) -> list[dict]:
+        """Per-step log of the last finalized session (part, slot, wait/kernel/D2H ms, D2H bytes)."""
+        arr = (L.SessionStep * L.K_LIMIT)()
+        cnt = C.c_uint32(0)
+        check(lib().gck_get_session_steps(self._ctx, arr, L.K_LIMIT, C.byref(cnt)), self._ctx)
+        return [arr[i].as_dict() for i in range(cnt.value)]
+
     def stats(self) -> dict:
         s = L.Stats()
         check(lib().gck_get_stats(self._ctx, C.byref(s)))

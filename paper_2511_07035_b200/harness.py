@@ -29,60 +29,75 @@ MODELS = {
     "llama2-7b": (6_738_415_616, 4096, 32, 32, 11008, 32000, True, 4096),
     "llama2-13b": (13_015_864_320, 5120, 40, 40, 13824, 32000, True, 4096),
 }
+FLAT_1M = 1 << 20  # BASELINE config 1: a flat fp32 vector, F/B = a spin kernel (SpinStandIn)
+
+
+def standin_shapes(model: str, tokens: int):
+    """The GEMMs of one decoder-only training step of `model` on `tokens` tokens: a list of
+    (kind, shape, repeat) with kind "mm" (M, K, N) or "bmm" (batch, M, K, N), forward order."""
+    _, d, layers, heads, ffn, vocab, gated, mseq = MODELS[model]
+    seq = min(mseq, tokens)
+    T, B = tokens, max(1, tokens // seq)
+    hd = d // heads
+    return [("mm", (T, d, 3 * d), layers),                      # qkv
+            ("bmm", (B * heads, seq, hd, seq), layers),          # q k^T
+            ("bmm", (B * heads, seq, seq, hd), layers),          # p v
+            ("mm", (T, d, d), layers),                          # attn out
+            ("mm", (T, d, (2 if gated else 1) * ffn), layers),  # fc (gate+up when gated)
+            ("mm", (T, ffn, d), layers),                        # down / proj
+            ("mm", (T, d, vocab), 1)]                           # lm head
+
+
+def standin_flops(model: str, tokens: int) -> int:
+    """FLOPs of one stand-in step (forward + dgrad + wgrad = 3 x 2MKN per GEMM); host-only."""
+    f = 0
+    for kind, sh, rep in standin_shapes(model, tokens):
+        M, K, N = sh[-3:]
+        f += rep * 3 * 2 * M * K * N * (sh[0] if kind == "bmm" else 1)
+    return f
 
 
 class TransformerGemmStandIn:
     """Every GEMM of one decoder-only transformer training step (forward, dgrad, wgrad) on
-    fixed random bf16 operands, in a CUDA graph: the F/B the checkpoint overlaps (harness).
+    fixed random bf16 operands, in CUDA graphs: the F/B the checkpoint overlaps (harness).
 
-    Shapes follow the named model (MODELS); attention score/value products are batched
+    Shapes follow the named model (standin_shapes); attention score/value products are batched
     GEMMs over heads. Layers share one set of operand buffers (same FLOPs and shapes,
     1/layers of the memory). cuBLAS library GEMMs, not part of the checkpoint path.
+    capture(bwd_parts=P) splits the backward into P graphs (each op's layer repeats divided
+    evenly), so gradient buckets can be reduce-scattered while the rest of the backward runs.
     """
 
-    def __init__(self, model: str = "gpt2-small", tokens: int = 16 * 1024, device="cuda", seed: int = 0,
-                 seq: int | None = None):
-        _, d, layers, heads, ffn, vocab, gated, mseq = MODELS[model]
-        seq = min(seq or mseq, tokens)
+    def __init__(self, model: str = "gpt2-small", tokens: int = 16 * 1024, device="cuda", seed: int = 0):
         g = torch.Generator(device=device)
         g.manual_seed(seed)
         bf = torch.bfloat16
-        self.flops = 0
         self.ops = []  # (kind, A, B, C, dA, dB, repeat)
-        T, B = tokens, max(1, tokens // seq)
         self.model, self.tokens = model, tokens
+        self.flops = standin_flops(model, tokens)
 
         def rnd(*shape):
             return (torch.randn(*shape, generator=g, device=device, dtype=torch.float32) * 0.02).to(bf)
 
-        def gemm(M, K, N, rep):
-            A, Bm = rnd(M, K), rnd(K, N)
-            C = torch.empty(M, N, device=device, dtype=bf)
-            self.ops.append(("mm", A, Bm, C, torch.empty_like(A), torch.empty_like(Bm), rep))
-            self.flops += rep * 3 * 2 * M * K * N
+        for kind, sh, rep in standin_shapes(model, tokens):
+            if kind == "mm":
+                M, K, N = sh
+                A, Bm, C = rnd(M, K), rnd(K, N), torch.empty(M, N, device=device, dtype=bf)
+            else:
+                Bt, M, K, N = sh
+                A, Bm, C = rnd(Bt, M, K), rnd(Bt, K, N), torch.empty(Bt, M, N, device=device, dtype=bf)
+            self.ops.append((kind, A, Bm, C, torch.empty_like(A), torch.empty_like(Bm), rep))
+        self.graphs = None
+        self.bwd_parts = 1
 
-        def bgemm(Bt, M, K, N, rep):
-            A, Bm = rnd(Bt, M, K), rnd(Bt, K, N)
-            C = torch.empty(Bt, M, N, device=device, dtype=bf)
-            self.ops.append(("bmm", A, Bm, C, torch.empty_like(A), torch.empty_like(Bm), rep))
-            self.flops += rep * 3 * 2 * Bt * M * K * N
-
-        hd = d // heads
-        gemm(T, d, 3 * d, layers)                  # qkv
-        bgemm(B * heads, seq, hd, seq, layers)     # q k^T
-        bgemm(B * heads, seq, seq, hd, layers)     # p v
-        gemm(T, d, d, layers)                      # attn out
-        gemm(T, d, (2 if gated else 1) * ffn, layers)  # fc (gate+up when gated)
-        gemm(T, ffn, d, layers)                    # down / proj
-        gemm(T, d, vocab, 1)                       # lm head
-        self.graph = None
-
-    def _run(self):
-        for kind, A, Bm, C, dA, dB, rep in self.ops:               # forward
+    def _forward(self):
+        for kind, A, Bm, C, dA, dB, rep in self.ops:
             for _ in range(rep):
                 (torch.mm if kind == "mm" else torch.bmm)(A, Bm, out=C)
-        for kind, A, Bm, C, dA, dB, rep in reversed(self.ops):     # backward: dgrad + wgrad
-            for _ in range(rep):
+
+    def _backward(self, part: int = 0, parts: int = 1):
+        for kind, A, Bm, C, dA, dB, rep in reversed(self.ops):   # dgrad + wgrad, last layer first
+            for _ in range(rep * part // parts, rep * (part + 1) // parts):
                 if kind == "mm":
                     torch.mm(C, Bm.t(), out=dA)
                     torch.mm(A.t(), C, out=dB)
@@ -90,23 +105,79 @@ class TransformerGemmStandIn:
                     torch.bmm(C, Bm.transpose(1, 2), out=dA)
                     torch.bmm(A.transpose(1, 2), C, out=dB)
 
-    def capture(self):
+    def _run(self):
+        self._forward()
+        for k in range(self.bwd_parts):
+            self._backward(k, self.bwd_parts)
+
+    def capture(self, bwd_parts: int = 1):
+        self.bwd_parts = max(1, bwd_parts)
         s = torch.cuda.Stream()
         s.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(s):
             for _ in range(2):
                 self._run()
         torch.cuda.current_stream().wait_stream(s)
-        self.graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.graph):
-            self._run()
+        self.graphs = []
+        for k in range(-1, self.bwd_parts):
+            gph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gph):
+                if k < 0:
+                    self._forward()
+                else:
+                    self._backward(k, self.bwd_parts)
+            self.graphs.append(gph)
         torch.cuda.synchronize()
 
-    def __call__(self):
-        if self.graph is None:
-            self._run()
+    def forward(self):
+        if self.graphs is None:
+            self._forward()
         else:
-            self.graph.replay()
+            self.graphs[0].replay()
+
+    def backward(self, part: int):
+        if self.graphs is None:
+            self._backward(part, self.bwd_parts)
+        else:
+            self.graphs[1 + part].replay()
+
+    def __call__(self):
+        self.forward()
+        for k in range(self.bwd_parts):
+            self.backward(k)
+
+
+class SpinStandIn:
+    """A fixed-duration F/B stand-in (BASELINE config 1: "spin kernel 1 ms (and 0)"): one
+    torch.cuda._sleep spin kernel of `ms` at the device's clock; ms = 0 launches nothing."""
+
+    def __init__(self, ms: float, device="cuda"):
+        self.ms = ms
+        self.flops = 0
+        self.bwd_parts = 1
+        rate_khz = torch.cuda.get_device_properties(device).clock_rate if ms > 0 else 0
+        self.cycles = int(ms * rate_khz)  # kHz x ms = cycles
+
+    def capture(self, bwd_parts: int = 1):
+        pass
+
+    def forward(self):
+        if self.cycles:
+            torch.cuda._sleep(self.cycles)
+
+    def backward(self, part: int):
+        pass
+
+    def __call__(self):
+        self.forward()
+
+
+def rs_buckets(n: int, world: int, bucket_bytes: int = 512 << 20, align: int = 512):
+    """ZeRO-1 gradient reduce-scatter buckets: (offset, count) ranges of the rank's n-element shard,
+    each the output of one reduce_scatter_tensor whose input (world x count bf16, laid out
+    contiguously per bucket) is about bucket_bytes. Covers [0, n) in order."""
+    cnt = max(align, (bucket_bytes // (2 * world)) // align * align)
+    return [(o, min(cnt, n - o)) for o in range(0, n, cnt)]
 
 
 def Gpt2GemmStandIn(tokens: int = 16 * 1024, device="cuda", seed: int = 0):

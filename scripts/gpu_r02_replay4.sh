@@ -1,0 +1,20 @@
+#!/bin/bash
+# Replay kernel v4 (3-way unrolled gradient pipeline, optional cp.async state prefetch, 3 vs 4 CTAs/SM);
+# the n > 2^32 tests; the bench N>1 relaunch + flat-1m tests.
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" || exit 1
+out=gpurun_out/r02_replay4.jsonl; : > $out
+for cfg in "t 3" "t 4" "u 3" "u 4" "r 3"; do
+  set -- $cfg; impl=$1; mb=$2
+  for nk in "124439808 8" "124439808 4" "124439808 16" "842301952 8"; do
+    set -- $nk
+    r=$(GCK_REPLAY_IMPL=$impl GCK_REPLAY_MINB=$mb GCK_N=$1 GCK_K=$2 timeout 300 python scripts/microbench_replay.py 2>&1 | tail -1)
+    echo "{\"impl\": \"$impl\", \"minb\": $mb, \"r\": $r}" >> $out
+  done
+done
+cat $out
+timeout 600 ncu --set full --import-source on --clock-control none -k regex:replay -s 2 -c 1 \
+   -o gpurun_out/replay_v4 -f python scripts/microbench_replay.py > gpurun_out/ncu_replay_v4.log 2>&1; echo "ncu rc=$?"
+timeout 1800 python -m pytest tests/test_gpu_guard.py tests/test_gpu_parity.py tests/test_gpu_fullsize.py tests/test_gpu_faults.py -q -m gpu -x 2>&1 | tail -5 | tee gpurun_out/r02_replay4_tests.txt
+timeout 1800 python -m pytest tests/test_gpu_huge.py tests/test_gpu_dist_smoke.py -q -m gpu -x 2>&1 | tail -15 | tee gpurun_out/r02_huge_dist_tests.txt
+free -g | head -2

@@ -25,8 +25,10 @@ for i in range(K - 1):
     G.h_generate(4, t, 1, 101 + i, 0, 1, 4)
     glog.append(t)
 alg = sum((hi - lo) * (24 + 2 * (K - 1 - j)) for j, (lo, hi) in enumerate(parts[:-1]))
+from paper_2511_07035_b200.harness import ClockSampler  # noqa: E402
+clocks = ClockSampler(0).start()
 ts = []
-for it in range(12):
+for it in range(22):
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record()
     G.replay_device(recs, parts, p, m, v, glog)
@@ -35,5 +37,6 @@ for it in range(12):
     if it >= 2:
         ts.append(a.elapsed_time(b))
 mean = statistics.mean(ts) / 1e3
+clk = clocks.stop()
 print(json.dumps({"n": n, "K": K, "element_updates": sum((hi - lo) * (K - 1 - j) for j, (lo, hi) in enumerate(parts[:-1])),
-                  "alg_bytes": alg, "us_mean": mean * 1e6, "gbs": alg / mean / 1e9, "frac_of_6500": alg / mean / 1e9 / 6500.6}))
+                  "alg_bytes": alg, "us_mean": mean * 1e6, "us_min": min(ts) * 1e3, "sm_mhz": clk.get("sm_mhz"), "gbs": alg / mean / 1e9, "frac_of_6500": alg / mean / 1e9 / 6500.6}))

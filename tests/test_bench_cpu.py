@@ -28,12 +28,50 @@ def test_reference_arm_json_line():
     assert d["config"]["workload"].startswith("GPT-2 small")
     assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["cores"] >= 1
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["value"] == d["value"]
+    cb = d["cpu_baseline"]
+    assert cb["sample_elements"] == 1 << 18 and cb["samples_timed"] == 2
+    assert abs(cb["measured_s_per_interval_sample"] * cb["extrapolation_factor"] - cb["extrapolated_s_per_interval"]) < 1e-9
 
 
 def test_reference_arm_other_ranks_exit_quietly():
-    out = run(["--impl", "reference", "--steps", "1", "--warmup", "1", "--cpu-sample", str(1 << 16)],
+    out = run(["--impl", "reference", "--gpus", "2", "--steps", "1", "--warmup", "1", "--cpu-sample", str(1 << 16)],
               env={"WORLD_SIZE": "2", "RANK": "1", "LOCAL_RANK": "1"})
     assert out.strip() == ""
+
+
+def test_gpus_must_match_world_size():
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "4"],
+                       capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, WORLD_SIZE="2", RANK="0", LOCAL_RANK="0"))
+    assert r.returncode != 0 and "WORLD_SIZE=2" in r.stderr
+
+
+def test_gpus_n_without_torchrun_relaunches_itself():
+    """`python bench.py --gpus 2` with no torchrun environment re-executes under
+    torch.distributed.run (2 local ranks over gloo here) and prints exactly one line, n_gpus == 2."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR",
+                                                             "MASTER_PORT")}
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--gpus", "2",
+                        "--dist-backend", "gloo", "--steps", "1", "--warmup", "0", "--cpu-sample", str(1 << 16),
+                        "--interval", "6", "--K", "2"],
+                       capture_output=True, text=True, timeout=600, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1 and lines[0]["n_gpus"] == 2 and lines[0]["impl"] == "reference"
+
+
+def test_reference_and_gpu_arm_share_the_config():
+    """The driver pairs the two arms by config: both lines build it with config_dict (the GPU arm
+    only overrides K with the K it used, equal to --K unless --K 0)."""
+    sys.path.insert(0, ROOT)
+    import importlib
+    bench = importlib.import_module("bench")
+    a = type("A", (), dict(model="gpt2-small", shard_of=0, n=0, tokens=0, K=8, interval=50, copy_mode="ce",
+                           ring_slots=2, staging="ring", scheme="gockpt", replay_mode="host",
+                           dist_backend="nccl", rs_bucket_mb=512, spin_ms=1.0))()
+    bench.resolve(a)
+    c1 = bench.config_dict(a, 1)
+    assert dict(c1, K=8) == c1 and c1["fb_tflop_per_step"] > 10 and c1["n_per_rank"] == 124_439_808
 
 
 def test_resolve_shards():

@@ -59,3 +59,36 @@ def test_one_gpu_bench_line_with_e2e(staging):
     e = d["e2e"]
     assert e["value"] > 0 and e["h2d_bytes_per_step"] == 2 * (1 << 24) and e["d2h_bytes_per_step"] > 8
     assert d["stall"]["session_steps_measured"] == 2 * 4 and d["gpu_launches"] > 0
+
+
+def test_gpus_2_without_torchrun_relaunches():
+    """`python bench.py --gpus 2` exactly as a user types it (no torchrun environment): bench.py
+    re-executes itself under torch.distributed.run; one line, n_gpus == 2, per-rank lists of 2."""
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2", "--dist-backend", "gloo", "--steps", "2",
+           "--warmup", "3", "--interval", "12", "--no-e2e"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = lines[0]
+    assert d["n_gpus"] == 2 and len(d["per_rank"]["ranks"]) == 2
+    assert d["d2h"]["link_peak_alone_gbs"] > 0 and d["d2h"]["link_peak_concurrent_gbs"] > 0
+
+
+def test_flat_1m_line_and_step_log(tmp_path):
+    """BASELINE config 1 as a bench line (F/B = a 1 ms spin kernel) with the per-step JSONL log."""
+    log = tmp_path / "steps.jsonl"
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--model", "flat-1m", "--K", "4", "--interval", "10",
+           "--steps", "3", "--warmup", "3", "--spin-ms", "1", "--step-log", str(log), "--no-cpu-baseline"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")][0]
+    assert d["unit"] == "steps/s" and d["config"]["n_per_rank"] == 1 << 20 and d["config"]["K"] == 4
+    assert d["config"]["workload"].startswith("flat 1M")
+    recs = [json.loads(l) for l in open(log)]
+    assert len(recs) == 3 * 10 - 1
+    assert [r_["part"] for r_ in recs[:10]] == [1, 2, 3, 4, 0, 0, 0, 0, 0, 0]
+    sess = [r_ for r_ in recs if r_["part"]]
+    assert all(r_["d2h_bytes"] > 0 and r_["fused_ms"] > 0 and r_["slot"] in (0, 1) for r_ in sess)
+    assert sum(r_["d2h_bytes"] for r_ in recs[:10]) == d["d2h"]["bytes_per_session"]

@@ -50,7 +50,8 @@ def test_struct_layouts_match_c(G, repo_root, tmp_path):
     structs = {"gck_hparams": L.Hparams, "gck_config": L.Config, "gck_tensors": L.Tensors,
                "gck_step_args": L.StepArgs, "gck_step_record": L.StepRecord, "gck_checkpoint": L.Checkpoint,
                "gck_staged": L.Staged, "gck_stats": L.Stats, "gck_file_header": L.FileHeader,
-               "gck_persist_stats": L.PersistStats, "gck_log_header": L.LogHeader}
+               "gck_persist_stats": L.PersistStats, "gck_log_header": L.LogHeader,
+               "gck_session_step": L.SessionStep}
     src = tmp_path / "sz.c"
     lines = ['#include <stdio.h>', '#include <stddef.h>', '#include "gockpt.h"', "int main(void){"]
     for cname, py in structs.items():
