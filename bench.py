@@ -96,6 +96,9 @@ def parse():
     ap.add_argument("--rs-bucket-mb", type=int, default=512,
                     help="N > 1 with NCCL: gradient reduce-scatter bucket size (input bytes), issued per "
                          "bucket while the rest of the backward stand-in runs")
+    ap.add_argument("--verify-drain", type=int, default=1,
+                    help="1 (library default): checksum every drained slice on the device and the host "
+                         "(a3 verification); 0: off")
     ap.add_argument("--step-log", default="",
                     help="write one JSON line per timed training step to this path (rank-suffixed when N > 1)")
     return ap.parse_args()
@@ -209,6 +212,26 @@ def oracle_baseline(args, K, steps=1, warmup=0):
             "samples_timed": len(times)}
 
 
+def host_info():
+    """The run header of the bench line: CPU model, cores, sockets, NUMA nodes of the box."""
+    model, sockets = None, set()
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name") and model is None:
+                    model = line.split(":", 1)[1].strip()
+                elif line.startswith("physical id"):
+                    sockets.add(line.split(":", 1)[1].strip())
+    except OSError:
+        pass
+    try:
+        nodes = len([d for d in os.listdir("/sys/devices/system/node") if d.startswith("node") and d[4:].isdigit()])
+    except OSError:
+        nodes = None
+    return {"cpu_model": model, "logical_cpus": os.cpu_count(), "affinity_cpus": len(os.sched_getaffinity(0)),
+            "sockets": len(sockets) or None, "numa_nodes": nodes}
+
+
 def unit_of(args):
     return "steps/s" if args.model == "flat-1m" else "tokens/s"
 
@@ -223,6 +246,7 @@ def config_dict(args, world):
             "fb_standin": fb,
             "fb_tflop_per_step": 0.0 if args.model == "flat-1m" else standin_flops(args.model, args.tokens) / 1e12,
             "copy_mode": args.copy_mode, "ring_slots": args.ring_slots, "staging": args.staging,
+            "verify_drain": bool(args.verify_drain),
             "scheme": args.scheme, "replay_mode": args.replay_mode,
             "dist_backend": args.dist_backend if world > 1 else None,
             "rs_bucket_mb": args.rs_bucket_mb if world > 1 and args.dist_backend == "nccl" else None,
@@ -263,6 +287,7 @@ def run_reference(args):
                             "(cpu_baseline); the measured wall time of this run is cpu_baseline.wall_s",
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": config_dict(args, world),
+        "host": host_info(),
         "cpu_baseline": cpu,
         "e2e": {"value": value, "unit": unit_of(args), "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -340,7 +365,7 @@ def main():
                    part_align=1024,
                    ring_slots=args.ring_slots, copy_mode=args.copy_mode, replay_threads=args.replay_threads,
                    timing=True, eager_replay=True, staging=args.staging, replay_mode=args.replay_mode,
-                   stream_buffers=args.stream_buffers)
+                   stream_buffers=args.stream_buffers, verify_drain=bool(args.verify_drain))
     baseline = args.scheme != "gockpt"
     if baseline:
         snap_host = [torch.empty(n, dtype=torch.float32, pin_memory=True) for _ in range(3)]
@@ -631,6 +656,7 @@ def main():
         "dtype": "f32",
         "data": "synthetic",
         "config": dict(config_dict(args, world), K=K),
+        "host": host_info(),
         "stall": {"wait_ms_per_session_step": stall_wait_ms / (args.steps * K),
                   "wait_ms_max": st1["stall_ms_max"],
                   "session_step_ms_median": statistics.median(sess_ms),
@@ -672,6 +698,7 @@ def main():
                   "auto_link_gbs": ctx_stats_final.get("auto_link_gbs"),
                   "note": "gck_recommend_k(n, measured link GB/s, checkpoint-free step time)"},
         "replay": {"host_ms_last_session": st1["last_replay_ms"], "threads": st1["replay_threads"],
+                   "verify_ms_last_session": st1.get("last_verify_ms"),
                    "worker_ms_last_session": st1["last_worker_ms"],
                    "finalize_wait_ms_last": st1["last_finalize_wait_ms"], "mode": args.replay_mode,
                    "stream_wait_ms_last": st1.get("last_stream_wait_ms"),

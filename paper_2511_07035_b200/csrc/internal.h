@@ -42,17 +42,11 @@ struct ReplayArgs {
 struct ReplayPlan {
     float *p, *m, *v;
     uint64_t n_replay;
-    uint32_t nact;
-    float neg_zero;  // -0.0f, passed at run time (adamw_group_p2's opaque nz)
+    uint32_t nact, _pad;
     uint64_t hi[GCK_K_LIMIT];
     uint32_t first[GCK_K_LIMIT];
     const uint16_t *glog[GCK_K_LIMIT];
     gck_step_record rec[GCK_K_LIMIT];
-    // mixed schedule (replay_kernel kMixed): segment s pairs part a (K-1-a pending updates) with part
-    // b = K-2-a (a+1 pending) and alternates their 32-group units; u0 = first unit of the segment
-    uint32_t nseg;
-    uint32_t seg_a[GCK_K_LIMIT], seg_b[GCK_K_LIMIT], seg_na[GCK_K_LIMIT], seg_nb[GCK_K_LIMIT];
-    uint64_t seg_u0[GCK_K_LIMIT + 1];
 };
 
 // Up to 4 (src, dst, bytes) sections drained by the zero-copy kernel (a3 variant).

@@ -593,39 +593,17 @@ __global__ void __launch_bounds__(256) replay_generic_kernel(const ReplayArgs a)
 // the groups with the part index tracked monotonically (one compare per group); every group lies in
 // one part (boundaries are multiples of 8, checked on the host). The update is adamw_group_mm:
 // the fused kernel's op sequence, one min/max guard per group and step.
-template <bool kUnitGs, bool kAllFast, bool kPacked, int kMinB = 1, bool kMixed = false>
-__global__ void __launch_bounds__(256, kMinB) replay_kernel(const ReplayPlan a) {
+template <bool kUnitGs, bool kAllFast>
+__global__ void __launch_bounds__(256) replay_kernel(const ReplayPlan a) {
     __shared__ RecP srec[GCK_K_LIMIT];
-    __shared__ __align__(16) RecF2 srec2[GCK_K_LIMIT];
-    for (uint32_t q = threadIdx.x; q < a.nact; q += blockDim.x) {
-        srec[q].f = to_recf(a.rec[q]);
-        srec2[q] = to_recf2(srec[q].f, a.neg_zero);
-    }
+    for (uint32_t q = threadIdx.x; q < a.nact; q += blockDim.x) srec[q].f = to_recf(a.rec[q]);
     __syncthreads();
-    const uint64_t ngroups = kMixed ? (a.seg_u0[a.nseg] << 5) : (a.n_replay >> 3);
+    const uint64_t ngroups = a.n_replay >> 3;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    uint32_t j = 0, sg = 0;
+    uint32_t j = 0;
     for (uint64_t gi = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; gi < ngroups; gi += stride) {
-        uint64_t e;
-        if (kMixed) {  // warp-uniform 32-group units, heavy and light parts alternating
-            const uint64_t u = gi >> 5;
-            while (u >= a.seg_u0[sg + 1]) ++sg;
-            const uint64_t l = u - a.seg_u0[sg], na = a.seg_na[sg], nb = a.seg_nb[sg];
-            const uint64_t both = 2 * (na < nb ? na : nb);
-            uint64_t ui;
-            if (l < both) {
-                j = (l & 1) ? a.seg_b[sg] : a.seg_a[sg];
-                ui = l >> 1;
-            } else {
-                j = na > nb ? a.seg_a[sg] : a.seg_b[sg];
-                ui = both / 2 + (l - both);
-            }
-            e = (j ? a.hi[j - 1] : 0) + ((ui << 5) + (gi & 31)) * 8;
-            if (e >= a.hi[j]) continue;  // the part's last unit is partial
-        } else {
-            e = gi << 3;
-            while (e >= a.hi[j]) ++j;  // e only grows: amortised O(1)
-        }
+        const uint64_t e = gi << 3;
+        while (e >= a.hi[j]) ++j;  // e only grows: amortised O(1)
         const uint32_t q0 = a.first[j];
         if (q0 >= a.nact) continue;  // every pending update of this part was skipped: already S(T)
         Vec8 p = ld8(a.p + e), m = ld8(a.m + e), v = ld8(a.v + e);
@@ -635,437 +613,11 @@ __global__ void __launch_bounds__(256, kMinB) replay_kernel(const ReplayPlan a) 
             if (q + 1 < a.nact) gnext = *reinterpret_cast<const uint4 *>(a.glog[q + 1] + e);
             const uint32_t gb[8] = {gq.x & 0xFFFFu, gq.x >> 16, gq.y & 0xFFFFu, gq.y >> 16,
                                     gq.z & 0xFFFFu, gq.z >> 16, gq.w & 0xFFFFu, gq.w >> 16};
-            if (kPacked)
-                adamw_group_p2<8, kUnitGs, kAllFast>(p.x, m.x, v.x, gb, srec[q].f, srec2[q]);
-            else
-                adamw_group_mm<8, kUnitGs, kAllFast>(p.x, m.x, v.x, gb, srec[q].f);
+            adamw_group_mm<8, kUnitGs, kAllFast>(p.x, m.x, v.x, gb, srec[q].f);
         }
         st8(a.p + e, p);
         st8(a.m + e, m);
         st8(a.v + e, v);
-    }
-}
-
-// ---- replay_kernel with a per-thread asynchronous prefetch ring (default) ----
-// The same per-thread work as replay_kernel, but the loads it waits for are issued early into a
-// per-thread shared-memory ring with cp.async (LDGSTS, 16 B each; no registers held in flight):
-//   - the next group's p, m, v and its first D gradient vectors, right after this group's state has
-//     been read into registers (one group of lead time: the long-scoreboard stall at every group
-//     start of replay_kernel);
-//   - inside a group, the gradient of step k + D while step k computes (replay_kernel's one-step
-//     lead did not cover the HBM latency under load; ncu: 32% of warp samples waited there).
-// Every step commits exactly one cp.async group, so "the data of step k" is always the group
-// committed D steps earlier: cp.async.wait_group(D-1). Slots are [slot][thread] 16-B entries
-// (conflict-free LDS.128). A slot is refilled only after its previous value was consumed in a
-// register (a dependent instruction first), so the async write never races the LDS.
-__device__ __forceinline__ void cp_async16(void *smem_dst, const void *gsrc) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)), "l"(gsrc) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-template <int D>
-struct ReplayRing {
-    static constexpr int kSlots = 6 + 2 * D;  // p0 p1 m0 m1 v0 v1 | gradients: 2 areas x D
-    static constexpr int smem(int threads) { return kSlots * 16 * threads; }
-};
-
-template <bool kUnitGs, int D>
-__global__ void __launch_bounds__(256, 4) replay_ring_kernel(const ReplayPlan a) {
-    extern __shared__ __align__(16) uint4 ring[];
-    __shared__ RecP srec[GCK_K_LIMIT];
-    __shared__ __align__(16) RecF2 srec2[GCK_K_LIMIT];
-    for (uint32_t q = threadIdx.x; q < a.nact; q += blockDim.x) {
-        srec[q].f = to_recf(a.rec[q]);
-        srec2[q] = to_recf2(srec[q].f, a.neg_zero);
-    }
-    __syncthreads();
-    const uint32_t T = blockDim.x;
-    uint4 *slot = ring + threadIdx.x;  // slot s of this thread: slot[s * T]
-    const uint64_t ngroups = a.n_replay >> 3;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    // issue the state + first D gradients of group gi into gradient area `area`; one commit
-    uint32_t jn = 0;  // part tracker of the prefetch cursor (groups only grow)
-    auto issue_group = [&](uint64_t gi, int area) {
-        if (gi < ngroups) {
-            const uint64_t e = gi << 3;
-            while (e >= a.hi[jn]) ++jn;
-            const uint32_t q0 = a.first[jn];
-            if (q0 < a.nact) {
-                cp_async16(&slot[0 * T], a.p + e);
-                cp_async16(&slot[1 * T], a.p + e + 4);
-                cp_async16(&slot[2 * T], a.m + e);
-                cp_async16(&slot[3 * T], a.m + e + 4);
-                cp_async16(&slot[4 * T], a.v + e);
-                cp_async16(&slot[5 * T], a.v + e + 4);
-                const uint32_t nst = a.nact - q0;
-#pragma unroll
-                for (int k = 0; k < D; ++k)
-                    if ((uint32_t)k < nst) cp_async16(&slot[(6 + area * D + k) * T], a.glog[q0 + k] + e);
-            }
-        }
-        cp_async_commit();
-    };
-    uint64_t gi = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    issue_group(gi, 0);
-    uint32_t j = 0;
-    int area = 0;
-    for (; gi < ngroups; gi += stride, area ^= 1) {
-        const uint64_t e = gi << 3;
-        while (e >= a.hi[j]) ++j;
-        const uint32_t q0 = a.first[j];
-        cp_async_wait<0>();  // this group's batch (issued one group ago) has landed
-        float p[8], m[8], v[8];
-        const bool live = q0 < a.nact;
-        if (live) {
-            const uint4 s0 = slot[0 * T], s1 = slot[1 * T], s2 = slot[2 * T], s3 = slot[3 * T], s4 = slot[4 * T],
-                        s5 = slot[5 * T];
-            const uint4 q4[6] = {s0, s1, s2, s3, s4, s5};
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                p[4 * h] = __uint_as_float(q4[h].x), p[4 * h + 1] = __uint_as_float(q4[h].y);
-                p[4 * h + 2] = __uint_as_float(q4[h].z), p[4 * h + 3] = __uint_as_float(q4[h].w);
-                m[4 * h] = __uint_as_float(q4[2 + h].x), m[4 * h + 1] = __uint_as_float(q4[2 + h].y);
-                m[4 * h + 2] = __uint_as_float(q4[2 + h].z), m[4 * h + 3] = __uint_as_float(q4[2 + h].w);
-                v[4 * h] = __uint_as_float(q4[4 + h].x), v[4 * h + 1] = __uint_as_float(q4[4 + h].y);
-                v[4 * h + 2] = __uint_as_float(q4[4 + h].z), v[4 * h + 3] = __uint_as_float(q4[4 + h].w);
-            }
-            uint32_t dep = s0.x ^ s1.x ^ s2.x ^ s3.x ^ s4.x ^ s5.x;  // the state slots are read: refill them
-            asm volatile("" : "+r"(dep)::"memory");
-        }
-        issue_group(gi + stride, area ^ 1);
-        if (!live) continue;  // every pending update of this part was skipped: already S(T)
-        const uint32_t nst = a.nact - q0;
-        for (uint32_t k = 0; k < nst; ++k) {
-            if (k >= (uint32_t)D) cp_async_wait<D - 1>();  // step k's gradient: committed D steps ago
-            uint4 *gs = &slot[(6 + area * D + (k % D)) * T];
-            const uint4 gq = *gs;
-            if (k + D < nst) {
-                uint32_t dep = gq.x;
-                asm volatile("" : "+r"(dep)::"memory");
-                cp_async16(gs, a.glog[q0 + k + D] + e);
-            }
-            cp_async_commit();
-            const uint32_t gb[8] = {gq.x & 0xFFFFu, gq.x >> 16, gq.y & 0xFFFFu, gq.y >> 16,
-                                    gq.z & 0xFFFFu, gq.z >> 16, gq.w & 0xFFFFu, gq.w >> 16};
-            adamw_group_p2<8, kUnitGs, false>(p, m, v, gb, srec[q0 + k].f, srec2[q0 + k]);
-        }
-        *reinterpret_cast<float4 *>(a.p + e) = make_float4(p[0], p[1], p[2], p[3]);
-        *reinterpret_cast<float4 *>(a.p + e + 4) = make_float4(p[4], p[5], p[6], p[7]);
-        *reinterpret_cast<float4 *>(a.m + e) = make_float4(m[0], m[1], m[2], m[3]);
-        *reinterpret_cast<float4 *>(a.m + e + 4) = make_float4(m[4], m[5], m[6], m[7]);
-        *reinterpret_cast<float4 *>(a.v + e) = make_float4(v[0], v[1], v[2], v[3]);
-        *reinterpret_cast<float4 *>(a.v + e + 4) = make_float4(v[4], v[5], v[6], v[7]);
-    }
-    cp_async_wait<0>();
-}
-
-// ---- replay_kernel, 3-way unrolled step loop (default) ----
-// As replay_kernel, with the gradient vectors in three rotating register sets: step k computes with
-// set k % 3 while the loads of steps k+1 and k+2 are in flight (two steps of lead instead of one;
-// ncu showed replay_kernel's warps waiting on the one-step prefetch at the end of every step), and
-// no register moves between steps. kPrefState: the next group's p, m, v are prefetched into a
-// per-thread shared-memory slot with cp.async while this group computes (the other long-scoreboard
-// wait of replay_kernel: the state loads at every group start).
-template <bool kUnitGs, bool kAllFast, bool kPrefState, int kMinBlocks>
-__global__ void __launch_bounds__(256, kMinBlocks) replay3_kernel(const ReplayPlan a) {
-    extern __shared__ __align__(16) uint4 sstate[];  // kPrefState: [6][blockDim] 16-B slots
-    __shared__ RecP srec[GCK_K_LIMIT];
-    __shared__ __align__(16) RecF2 srec2[GCK_K_LIMIT];
-    for (uint32_t q = threadIdx.x; q < a.nact; q += blockDim.x) {
-        srec[q].f = to_recf(a.rec[q]);
-        srec2[q] = to_recf2(srec[q].f, a.neg_zero);
-    }
-    __syncthreads();
-    const uint32_t T = blockDim.x;
-    uint4 *slot = sstate + threadIdx.x;
-    const uint64_t ngroups = a.n_replay >> 3;
-    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    uint32_t j = 0, jn = 0;
-    auto pref = [&](uint64_t gi) {  // next group's state -> slot (kPrefState); one commit
-        if (gi < ngroups) {
-            const uint64_t e = gi << 3;
-            while (e >= a.hi[jn]) ++jn;
-            if (a.first[jn] < a.nact) {
-                cp_async16(&slot[0 * T], a.p + e);
-                cp_async16(&slot[1 * T], a.p + e + 4);
-                cp_async16(&slot[2 * T], a.m + e);
-                cp_async16(&slot[3 * T], a.m + e + 4);
-                cp_async16(&slot[4 * T], a.v + e);
-                cp_async16(&slot[5 * T], a.v + e + 4);
-            }
-        }
-        cp_async_commit();
-    };
-    uint64_t gi = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (kPrefState) pref(gi);
-    for (; gi < ngroups; gi += stride) {
-        const uint64_t e = gi << 3;
-        while (e >= a.hi[j]) ++j;
-        const uint32_t q0 = a.first[j];
-        const bool live = q0 < a.nact;
-        float p[8], m[8], v[8];
-        if (kPrefState) {
-            cp_async_wait<0>();
-            if (live) {
-                const uint4 s0 = slot[0 * T], s1 = slot[1 * T], s2 = slot[2 * T], s3 = slot[3 * T],
-                            s4 = slot[4 * T], s5 = slot[5 * T];
-                const uint4 q4[6] = {s0, s1, s2, s3, s4, s5};
-#pragma unroll
-                for (int h = 0; h < 2; ++h) {
-                    p[4 * h] = __uint_as_float(q4[h].x), p[4 * h + 1] = __uint_as_float(q4[h].y);
-                    p[4 * h + 2] = __uint_as_float(q4[h].z), p[4 * h + 3] = __uint_as_float(q4[h].w);
-                    m[4 * h] = __uint_as_float(q4[2 + h].x), m[4 * h + 1] = __uint_as_float(q4[2 + h].y);
-                    m[4 * h + 2] = __uint_as_float(q4[2 + h].z), m[4 * h + 3] = __uint_as_float(q4[2 + h].w);
-                    v[4 * h] = __uint_as_float(q4[4 + h].x), v[4 * h + 1] = __uint_as_float(q4[4 + h].y);
-                    v[4 * h + 2] = __uint_as_float(q4[4 + h].z), v[4 * h + 3] = __uint_as_float(q4[4 + h].w);
-                }
-                uint32_t dep = s0.x ^ s1.x ^ s2.x ^ s3.x ^ s4.x ^ s5.x;  // slots read: refill them
-                asm volatile("" : "+r"(dep)::"memory");
-            }
-            pref(gi + stride);
-        }
-        if (!live) continue;  // every pending update of this part was skipped: already S(T)
-        const uint32_t nst = a.nact - q0;
-        const uint16_t *const *gl = a.glog + q0;
-        const RecP *rr = srec + q0;
-        uint4 g0 = *reinterpret_cast<const uint4 *>(gl[0] + e), g1 = make_uint4(0, 0, 0, 0), g2 = g1;
-        if (nst > 1) g1 = *reinterpret_cast<const uint4 *>(gl[1] + e);
-        if (!kPrefState) {
-            const Vec8 pv = ld8(a.p + e), mv = ld8(a.m + e), vv = ld8(a.v + e);
-#pragma unroll
-            for (int k = 0; k < 8; ++k) p[k] = pv.x[k], m[k] = mv.x[k], v[k] = vv.x[k];
-        }
-        const RecF2 *rr2 = srec2 + q0;
-        auto step = [&](const uint4 &gq, const RecF &r, const RecF2 &c) {
-            const uint32_t gb[8] = {gq.x & 0xFFFFu, gq.x >> 16, gq.y & 0xFFFFu, gq.y >> 16,
-                                    gq.z & 0xFFFFu, gq.z >> 16, gq.w & 0xFFFFu, gq.w >> 16};
-            adamw_group_p2<8, kUnitGs, kAllFast>(p, m, v, gb, r, c);
-        };
-        uint32_t k = 0;
-        for (; k + 3 <= nst; k += 3) {  // sets: step k -> g0, k+1 -> g1, k+2 -> g2
-            if (k + 2 < nst) g2 = *reinterpret_cast<const uint4 *>(gl[k + 2] + e);
-            step(g0, rr[k].f, rr2[k]);
-            if (k + 3 < nst) g0 = *reinterpret_cast<const uint4 *>(gl[k + 3] + e);
-            step(g1, rr[k + 1].f, rr2[k + 1]);
-            if (k + 4 < nst) g1 = *reinterpret_cast<const uint4 *>(gl[k + 4] + e);
-            step(g2, rr[k + 2].f, rr2[k + 2]);
-        }
-        if (k < nst) {  // 1 or 2 steps left, in g0 (and g1)
-            step(g0, rr[k].f, rr2[k]);
-            if (k + 1 < nst) step(g1, rr[k + 1].f, rr2[k + 1]);
-        }
-        *reinterpret_cast<float4 *>(a.p + e) = make_float4(p[0], p[1], p[2], p[3]);
-        *reinterpret_cast<float4 *>(a.p + e + 4) = make_float4(p[4], p[5], p[6], p[7]);
-        *reinterpret_cast<float4 *>(a.m + e) = make_float4(m[0], m[1], m[2], m[3]);
-        *reinterpret_cast<float4 *>(a.m + e + 4) = make_float4(m[4], m[5], m[6], m[7]);
-        *reinterpret_cast<float4 *>(a.v + e) = make_float4(v[0], v[1], v[2], v[3]);
-        *reinterpret_cast<float4 *>(a.v + e + 4) = make_float4(v[4], v[5], v[6], v[7]);
-    }
-    if (kPrefState) cp_async_wait<0>();
-}
-
-// ---- a5 GPU replay, TMA-pipelined (GCK_REPLAY_IMPL=b) ----
-// Persistent CTAs, one per SM. The stale range is cut into tiles of kTile elements that never
-// straddle a part. A load warp bulk-copies each tile's p, m, v into a state stage (kS deep) and the
-// tile's gradient slices, kGS steps per gradient chunk (kGd deep); kCW consumer warps read the stage
-// into registers, apply every pending update (adamw_group_p2) and write the results back into the
-// stage; a store warp bulk-stores the finished stage. Each CTA walks its round-robin tiles
-// alternately from the front (part 1: K-1 updates) and the back (part K-1: one update) so the ALU-
-// and HBM-heavy tiles overlap in the pipeline.
-template <int kTile, int kCW, int kS, int kGd, int kGS>
-struct ReplayTma {
-    static constexpr int kThreads = kCW * 32;
-    static constexpr int kQ = kTile / 4 / kThreads;  // float4 groups per consumer thread
-    static constexpr int kStateBytes = kTile * 12;
-    static constexpr int kChunkBytes = kTile * 2 * kGS;
-    static constexpr int smem() { return kS * kStateBytes + kGd * kChunkBytes + (3 * kS + 2 * kGd) * 8; }
-    static_assert(kQ * kThreads * 4 == kTile, "tile must split evenly");
-};
-
-struct ReplayTiles {  // per-CTA schedule in shared memory
-    uint32_t tstart[GCK_K_LIMIT + 1];  // tiles before part j (parts with no pending update: 0 tiles)
-    uint32_t nparts;
-};
-
-__device__ __forceinline__ uint32_t tile_part(const ReplayTiles &s, uint32_t t) {
-    uint32_t lo = 0, hi = s.nparts;  // largest j with tstart[j] <= t
-    while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (s.tstart[mid] <= t) lo = mid;
-        else hi = mid;
-    }
-    return lo;
-}
-
-__device__ __forceinline__ uint32_t cta_tile(uint32_t k, uint32_t nq) {
-    const uint32_t q = (k & 1u) ? (nq - 1u - (k >> 1)) : (k >> 1);
-    return blockIdx.x + q * gridDim.x;
-}
-
-template <int kTile, int kCW, int kS, int kGd, int kGS, bool kUnitGs>
-__global__ void __launch_bounds__((kCW + 2) * 32, 1) replay_tma_kernel(const ReplayPlan a) {
-    using C = ReplayTma<kTile, kCW, kS, kGd, kGS>;
-    extern __shared__ __align__(128) uint8_t smem[];
-    uint8_t *gbuf = smem + kS * C::kStateBytes;
-    uint64_t *full = reinterpret_cast<uint64_t *>(gbuf + kGd * C::kChunkBytes);
-    uint64_t *done = full + kS;
-    uint64_t *empty = done + kS;
-    uint64_t *gfull = empty + kS;
-    uint64_t *gempty = gfull + kGd;
-    __shared__ RecP srec[GCK_K_LIMIT];
-    __shared__ __align__(16) RecF2 srec2[GCK_K_LIMIT];
-    __shared__ ReplayTiles sch;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    uint32_t nparts = 0;
-    while (nparts < GCK_K_LIMIT && (nparts == 0 || a.hi[nparts - 1] < a.n_replay)) ++nparts;
-    if (threadIdx.x == 0) {
-        uint32_t tiles = 0;
-        for (uint32_t j = 0; j < nparts; ++j) {
-            sch.tstart[j] = tiles;
-            const uint64_t lo = j ? a.hi[j - 1] : 0;
-            if (a.first[j] < a.nact) tiles += (uint32_t)((a.hi[j] - lo + kTile - 1) / kTile);
-        }
-        sch.tstart[nparts] = tiles;
-        sch.nparts = nparts;
-        for (int s = 0; s < kS; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&done[s], kCW);
-            mbar_init(&empty[s], 1);
-        }
-        for (int g = 0; g < kGd; ++g) {
-            mbar_init(&gfull[g], 1);
-            mbar_init(&gempty[g], kCW);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    for (uint32_t q = threadIdx.x; q < a.nact; q += blockDim.x) {
-        srec[q].f = to_recf(a.rec[q]);
-        srec2[q] = to_recf2(srec[q].f, a.neg_zero);
-    }
-    __syncthreads();
-    const uint32_t ntiles = sch.tstart[nparts];
-    const uint32_t nq = blockIdx.x < ntiles ? (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
-    auto tile_of = [&](uint32_t k, uint32_t &j, uint64_t &base, uint32_t &len) {
-        const uint32_t t = cta_tile(k, nq);
-        j = tile_part(sch, t);
-        const uint64_t lo = j ? a.hi[j - 1] : 0;
-        base = lo + (uint64_t)(t - sch.tstart[j]) * kTile;
-        const uint64_t rem = a.hi[j] - base;
-        len = (uint32_t)(rem < (uint64_t)kTile ? rem : (uint64_t)kTile);
-    };
-    if (warp == kCW) {  // load warp
-        if (lane == 0) {
-            uint32_t gc = 0;
-            for (uint32_t k = 0; k < nq; ++k) {
-                uint32_t j, len;
-                uint64_t base;
-                tile_of(k, j, base, len);
-                const int s = k % kS;
-                mbar_wait(&empty[s], ((k / kS) & 1u) ^ 1u);
-                mbar_expect_tx(&full[s], len * 12);
-                uint8_t *st = smem + s * C::kStateBytes;
-                bulk_g2s(st, a.p + base, len * 4, &full[s]);
-                bulk_g2s(st + kTile * 4, a.m + base, len * 4, &full[s]);
-                bulk_g2s(st + kTile * 8, a.v + base, len * 4, &full[s]);
-                for (uint32_t q0 = a.first[j]; q0 < a.nact; q0 += kGS, ++gc) {
-                    const uint32_t nst = umin((uint32_t)kGS, a.nact - q0);
-                    const int g = gc % kGd;
-                    mbar_wait(&gempty[g], ((gc / kGd) & 1u) ^ 1u);
-                    mbar_expect_tx(&gfull[g], len * 2 * nst);
-                    uint8_t *gb = gbuf + g * C::kChunkBytes;
-                    for (uint32_t q = 0; q < nst; ++q)
-                        bulk_g2s(gb + q * kTile * 2, a.glog[q0 + q] + base, len * 2, &gfull[g]);
-                }
-            }
-        }
-        return;
-    }
-    if (warp == kCW + 1) {  // store warp
-        if (lane == 0) {
-            int prev = -1;
-            for (uint32_t k = 0; k < nq; ++k) {
-                uint32_t j, len;
-                uint64_t base;
-                tile_of(k, j, base, len);
-                const int s = k % kS;
-                mbar_wait(&done[s], (k / kS) & 1u);
-                const uint8_t *st = smem + s * C::kStateBytes;
-                bulk_s2g(a.p + base, st, len * 4);
-                bulk_s2g(a.m + base, st + kTile * 4, len * 4);
-                bulk_s2g(a.v + base, st + kTile * 8, len * 4);
-                bulk_commit();
-                bulk_wait_read_1();
-                if (prev >= 0) mbar_arrive(&empty[prev]);
-                prev = s;
-            }
-            bulk_wait_read();
-            if (prev >= 0) mbar_arrive(&empty[prev]);
-            bulk_wait_all();
-        }
-        return;
-    }
-    const int c = threadIdx.x;
-    uint32_t gc = 0;
-    for (uint32_t k = 0; k < nq; ++k) {
-        uint32_t j, len;
-        uint64_t base;
-        tile_of(k, j, base, len);
-        const int s = k % kS;
-        mbar_wait(&full[s], (k / kS) & 1u);
-        uint8_t *st = smem + s * C::kStateBytes;
-        float4 *sp = reinterpret_cast<float4 *>(st);
-        float4 *sm = reinterpret_cast<float4 *>(st + kTile * 4);
-        float4 *sv = reinterpret_cast<float4 *>(st + kTile * 8);
-        float p[4 * C::kQ], m[4 * C::kQ], v[4 * C::kQ];
-#pragma unroll
-        for (int q = 0; q < C::kQ; ++q) {
-            const int f = c + q * C::kThreads;
-            const float4 p4 = sp[f], m4 = sm[f], v4 = sv[f];  // lanes past len hold stale bytes, never stored
-            p[4 * q] = p4.x, p[4 * q + 1] = p4.y, p[4 * q + 2] = p4.z, p[4 * q + 3] = p4.w;
-            m[4 * q] = m4.x, m[4 * q + 1] = m4.y, m[4 * q + 2] = m4.z, m[4 * q + 3] = m4.w;
-            v[4 * q] = v4.x, v[4 * q + 1] = v4.y, v[4 * q + 2] = v4.z, v[4 * q + 3] = v4.w;
-        }
-        for (uint32_t q0 = a.first[j]; q0 < a.nact; q0 += kGS, ++gc) {
-            const uint32_t nst = umin((uint32_t)kGS, a.nact - q0);
-            const int g = gc % kGd;
-            mbar_wait(&gfull[g], (gc / kGd) & 1u);
-            const uint8_t *gbp = gbuf + g * C::kChunkBytes;
-            uint32_t dep = 0;
-            for (uint32_t q = 0; q < nst; ++q) {
-                const uint2 *gq = reinterpret_cast<const uint2 *>(gbp + q * kTile * 2);
-                uint32_t gbits[4 * C::kQ];
-#pragma unroll
-                for (int h = 0; h < C::kQ; ++h) {
-                    const uint2 g2 = gq[c + h * C::kThreads];
-                    dep ^= g2.x;
-                    gbits[4 * h] = g2.x & 0xFFFFu, gbits[4 * h + 1] = g2.x >> 16;
-                    gbits[4 * h + 2] = g2.y & 0xFFFFu, gbits[4 * h + 3] = g2.y >> 16;
-                }
-                adamw_group_p2<4 * C::kQ, kUnitGs, false>(p, m, v, gbits, srec[q0 + q].f, srec2[q0 + q]);
-            }
-            asm volatile("" : "+r"(dep));
-            __syncwarp();
-            if (lane == 0) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_arrive(&gempty[g]);
-            }
-        }
-#pragma unroll
-        for (int q = 0; q < C::kQ; ++q) {
-            const int f = c + q * C::kThreads;
-            if (4u * (uint32_t)f < len) {
-                sp[f] = make_float4(p[4 * q], p[4 * q + 1], p[4 * q + 2], p[4 * q + 3]);
-                sm[f] = make_float4(m[4 * q], m[4 * q + 1], m[4 * q + 2], m[4 * q + 3]);
-                sv[f] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-            }
-        }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&done[s]);
     }
 }
 
@@ -1325,7 +877,6 @@ static bool replay_plan(const ReplayArgs &a, ReplayPlan *rp, bool *unit_gs) {
     rp->m = a.m;
     rp->v = a.v;
     rp->n_replay = a.n_replay;
-    rp->neg_zero = -0.0f;
     *unit_gs = true;
     for (uint32_t i = 0; i + 1 < a.K; ++i) {
         if ((a.lo[i] | a.hi[i]) & 7u) return false;
@@ -1346,57 +897,8 @@ static bool replay_plan(const ReplayArgs &a, ReplayPlan *rp, bool *unit_gs) {
             rp->first[j] = q;
         }
     }
-    {  // mixed schedule: pair part a with part K-2-a (a+1 and K-1-a pending updates: K per pair)
-        const uint32_t P = a.K - 1;
-        uint64_t u = 0;
-        rp->nseg = 0;
-        for (uint32_t x = 0, y = P - 1; x <= y && P; ++x, --y) {
-            const uint32_t s = rp->nseg++;
-            auto units = [&](uint32_t jj) -> uint64_t {
-                if (rp->first[jj] >= rp->nact) return 0;
-                const uint64_t lo = jj ? a.hi[jj - 1] : 0;
-                return ((a.hi[jj] - lo) / 8 + 31) / 32;
-            };
-            rp->seg_a[s] = x;
-            rp->seg_b[s] = y;
-            rp->seg_na[s] = (uint32_t)units(x);
-            rp->seg_nb[s] = x == y ? 0 : (uint32_t)units(y);
-            rp->seg_u0[s] = u;
-            u += rp->seg_na[s] + rp->seg_nb[s];
-            if (y == 0) break;
-        }
-        rp->seg_u0[rp->nseg] = u;
-    }
     const char *e = getenv("GCK_REPLAY_IMPL");
     return (al & 15u) == 0 && !(e && e[0] == 's');
-}
-
-template <int kTile, int kCW, int kS, int kGd, int kGS>
-int launch_replay_tma(const ReplayPlan &rp, bool unit_gs, cudaStream_t s, int num_sms) {
-    using C = ReplayTma<kTile, kCW, kS, kGd, kGS>;
-    static std::atomic<uint64_t> attr_set_devices{0};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const uint64_t bit = 1ull << (dev & 63);
-    if (!(attr_set_devices.load() & bit)) {
-        cudaFuncSetAttribute(replay_tma_kernel<kTile, kCW, kS, kGd, kGS, true>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem());
-        cudaFuncSetAttribute(replay_tma_kernel<kTile, kCW, kS, kGd, kGS, false>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, C::smem());
-        attr_set_devices.fetch_or(bit);
-    }
-    uint64_t tiles = 0, lo = 0;
-    for (uint32_t j = 0; lo < rp.n_replay; ++j) {
-        if (rp.first[j] < rp.nact) tiles += (rp.hi[j] - lo + kTile - 1) / kTile;
-        lo = rp.hi[j];
-    }
-    if (!tiles) return 0;
-    const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, num_sms > 0 ? num_sms : 148));
-    if (unit_gs)
-        replay_tma_kernel<kTile, kCW, kS, kGd, kGS, true><<<grid, (kCW + 2) * 32, C::smem(), s>>>(rp);
-    else
-        replay_tma_kernel<kTile, kCW, kS, kGd, kGS, false><<<grid, (kCW + 2) * 32, C::smem(), s>>>(rp);
-    return (int)cudaGetLastError();
 }
 
 // the host mirror of to_recf's `fast` test for every record of the plan (kAllFast)
@@ -1410,120 +912,20 @@ static bool all_fast(const ReplayPlan &rp) {
     return true;
 }
 
-template <bool U, bool F, bool P, int B>
-int launch_replay3_b(const ReplayPlan &rp, cudaStream_t s, int num_sms) {
-    const int smem = P ? 6 * 16 * 256 : 0;  // 24 KiB: below the 48 KiB default, no opt-in needed
-    replay3_kernel<U, F, P, B><<<grid_for(rp.n_replay >> 3, 256, num_sms, B), 256, smem, s>>>(rp);
-    return (int)cudaGetLastError();
-}
-
-template <bool U, bool F, bool P>
-int launch_replay3_t(const ReplayPlan &rp, cudaStream_t s, int num_sms) {
-    const char *e = getenv("GCK_REPLAY_MINB");
-    return (e && e[0] == '4') ? launch_replay3_b<U, F, P, 4>(rp, s, num_sms) : launch_replay3_b<U, F, P, 3>(rp, s, num_sms);
-}
-
-static int launch_replay3(const ReplayPlan &rp, bool unit_gs, bool fast, bool pref_state, cudaStream_t s,
-                          int num_sms) {
-    const int sel = (unit_gs ? 4 : 0) | (fast ? 2 : 0) | (pref_state ? 1 : 0);
-    switch (sel) {
-        case 7: return launch_replay3_t<true, true, true>(rp, s, num_sms);
-        case 6: return launch_replay3_t<true, true, false>(rp, s, num_sms);
-        case 5: return launch_replay3_t<true, false, true>(rp, s, num_sms);
-        case 4: return launch_replay3_t<true, false, false>(rp, s, num_sms);
-        case 3: return launch_replay3_t<false, true, true>(rp, s, num_sms);
-        case 2: return launch_replay3_t<false, true, false>(rp, s, num_sms);
-        case 1: return launch_replay3_t<false, false, true>(rp, s, num_sms);
-        default: return launch_replay3_t<false, false, false>(rp, s, num_sms);
-    }
-}
-
-template <int D>
-int launch_replay_ring(const ReplayPlan &rp, bool unit_gs, cudaStream_t s, int num_sms) {
-    static std::atomic<uint64_t> attr_set_devices{0};  // the smem opt-in is per device
-    int dev = 0;
-    cudaGetDevice(&dev);
-    const uint64_t bit = 1ull << (dev & 63);
-    const int smem = ReplayRing<D>::smem(256);
-    if (!(attr_set_devices.load() & bit)) {
-        cudaFuncSetAttribute(replay_ring_kernel<true, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(replay_ring_kernel<false, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        attr_set_devices.fetch_or(bit);
-    }
-    const unsigned grid = grid_for(rp.n_replay >> 3, 256, num_sms, 4);
-    if (unit_gs)
-        replay_ring_kernel<true, D><<<grid, 256, smem, s>>>(rp);
-    else
-        replay_ring_kernel<false, D><<<grid, 256, smem, s>>>(rp);
-    return (int)cudaGetLastError();
-}
-
 int launch_replay(const ReplayArgs &a, void *stream, int num_sms) {
     if (a.n_replay == 0) return 0;
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     ReplayPlan rp;
     bool unit_gs = false;
     if (replay_plan(a, &rp, &unit_gs)) {
-        const char *e = getenv("GCK_REPLAY_IMPL");
-        if (e && (e[0] == '5' || e[0] == '6')) {  // packed, more resident CTAs (fewer registers)
-            const int mb = e[0] - '0';
-            const unsigned grid = grid_for(a.n_replay >> 3, 256, num_sms, mb);
-            if (mb == 5) {
-                if (unit_gs) replay_kernel<true, true, true, 5><<<grid, 256, 0, s>>>(rp);
-                else replay_kernel<false, true, true, 5><<<grid, 256, 0, s>>>(rp);
-            } else {
-                if (unit_gs) replay_kernel<true, true, true, 6><<<grid, 256, 0, s>>>(rp);
-                else replay_kernel<false, true, true, 6><<<grid, 256, 0, s>>>(rp);
-            }
-            return (int)cudaGetLastError();
+        const unsigned grid = grid_for(a.n_replay >> 3, 256, num_sms, 8);
+        switch ((unit_gs ? 2 : 0) | (all_fast(rp) ? 1 : 0)) {
+            case 3: replay_kernel<true, true><<<grid, 256, 0, s>>>(rp); break;
+            case 2: replay_kernel<true, false><<<grid, 256, 0, s>>>(rp); break;
+            case 1: replay_kernel<false, true><<<grid, 256, 0, s>>>(rp); break;
+            default: replay_kernel<false, false><<<grid, 256, 0, s>>>(rp); break;
         }
-        if (e && e[0] == 'x') {  // packed, heavy/light parts interleaved per 32-group unit
-            const unsigned grid = grid_for(a.n_replay >> 3, 256, num_sms, 8);
-            if (unit_gs) replay_kernel<true, true, true, 4, true><<<grid, 256, 0, s>>>(rp);
-            else replay_kernel<false, true, true, 4, true><<<grid, 256, 0, s>>>(rp);
-            return (int)cudaGetLastError();
-        }
-        if (e && e[0] == 'q') {  // packed, grid = 4 resident CTAs per SM exactly
-            const unsigned grid = grid_for(a.n_replay >> 3, 256, num_sms, 4);
-            if (unit_gs) replay_kernel<true, true, true><<<grid, 256, 0, s>>>(rp);
-            else replay_kernel<false, true, true><<<grid, 256, 0, s>>>(rp);
-            return (int)cudaGetLastError();
-        }
-        if (!e || e[0] == 'p' || e[0] == 'r') {  // default: packed pairs; 'r': scalar arithmetic
-            const bool packed = !(e && e[0] == 'r');
-            const unsigned grid = grid_for(a.n_replay >> 3, 256, num_sms, 8);
-            const int sel = (unit_gs ? 4 : 0) | (all_fast(rp) ? 2 : 0) | (packed ? 1 : 0);
-            switch (sel) {
-                case 7: replay_kernel<true, true, true><<<grid, 256, 0, s>>>(rp); break;
-                case 6: replay_kernel<true, true, false><<<grid, 256, 0, s>>>(rp); break;
-                case 5: replay_kernel<true, false, true><<<grid, 256, 0, s>>>(rp); break;
-                case 4: replay_kernel<true, false, false><<<grid, 256, 0, s>>>(rp); break;
-                case 3: replay_kernel<false, true, true><<<grid, 256, 0, s>>>(rp); break;
-                case 2: replay_kernel<false, true, false><<<grid, 256, 0, s>>>(rp); break;
-                case 1: replay_kernel<false, false, true><<<grid, 256, 0, s>>>(rp); break;
-                default: replay_kernel<false, false, false><<<grid, 256, 0, s>>>(rp); break;
-            }
-            return (int)cudaGetLastError();
-        }
-        if (e && e[0] == 'b') {  // TMA-pipelined (bulk copies, producer / consumer / store warps)
-            const char *t = getenv("GCK_REPLAY_TMA");
-            const int cfg = t ? atoi(t) : 0;
-            switch (cfg) {
-                case 1: return launch_replay_tma<2048, 16, 4, 3, 8>(rp, unit_gs, s, num_sms);
-                case 2: return launch_replay_tma<4096, 8, 3, 2, 4>(rp, unit_gs, s, num_sms);
-                case 3: return launch_replay_tma<2048, 8, 4, 3, 8>(rp, unit_gs, s, num_sms);
-                default: return launch_replay_tma<4096, 16, 3, 2, 4>(rp, unit_gs, s, num_sms);
-            }
-        }
-        if (e && e[0] == 'c') {  // the per-thread cp.async ring (state + D gradients ahead)
-            const char *dcfg = getenv("GCK_REPLAY_D");
-            const int D = dcfg ? atoi(dcfg) : 3;
-            return D == 2 ? launch_replay_ring<2>(rp, unit_gs, s, num_sms)
-                   : D == 4 ? launch_replay_ring<4>(rp, unit_gs, s, num_sms)
-                            : launch_replay_ring<3>(rp, unit_gs, s, num_sms);
-        }
-        const bool pref_state = !(e && e[0] == 'u');  // 'u': unrolled, state loaded at group start
-        return launch_replay3(rp, unit_gs, all_fast(rp), pref_state, s, num_sms);
+        return (int)cudaGetLastError();
     }
     const unsigned grid = grid_for((a.n_replay + 7) >> 3, 256, num_sms, 8);
     replay_generic_kernel<<<grid, 256, 0, s>>>(a);
