@@ -340,20 +340,22 @@ struct gck_ctx {
         return GCK_E_INCOMPLETE;
     }
 
-    // Host side of the drain verification for session step i (after done[i-1]): the checksums of
-    // the landed bytes against the device checksums of the staged bytes (taken on the D2H stream
-    // right before the copy). GCK_FAULT_FLIP=<i> corrupts one landed byte first (test hook).
-    gck_status verify_step(uint32_t i) {
+    // Compare session step i's landed sections with the device checksums of the staged bytes: from
+    // the replay's folded sums, or (sums == nullptr) by summing the landed bytes here.
+    gck_status verify_sections(uint32_t i, const gck::ReplayChecksums *sums) {
         const uint64_t lo = this->lo[i - 1], pe = hi[i - 1] - lo, ghi = (i < K) ? hi[i - 1] : 0;
-        if (fault_flip == i) reinterpret_cast<uint8_t *>(h_master + lo)[pe * 2] ^= 0x10u;
-        if (!verify) return GCK_OK;
         const void *sec[4] = {h_master + lo, h_m + lo, h_v + lo, glog[i - 1]};
         const uint64_t bytes[4] = {pe * 4, pe * 4, pe * 4, ghi * 2};
         static const char *names[4] = {"master", "exp_avg", "exp_avg_sq", "gradient"};
         for (int k = 0; k < 4; ++k) {
             if (!bytes[k]) continue;
             uint64_t a = 0, b = 0;
-            gck::checksum_host(sec[k], bytes[k], &a, &b, cfg.replay_threads, numa >= 0 ? &numa_cpus : nullptr);
+            if (sums) {
+                a = sums->a[i - 1][k];
+                b = sums->b[i - 1][k];
+            } else {
+                gck::checksum_host(sec[k], bytes[k], &a, &b, cfg.replay_threads, numa >= 0 ? &numa_cpus : nullptr);
+            }
             const unsigned long long *d = hsum + (uint64_t)(i - 1) * 8 + 2 * k;
             if (a != d[0] || b != d[1]) {
                 worker_error = "drain verification: session step " + std::to_string(i) + " " + names[k] +
@@ -362,6 +364,16 @@ struct gck_ctx {
             }
         }
         return GCK_OK;
+    }
+
+    // Host side of the drain verification for session step i (after done[i-1]): the checksums of
+    // the landed bytes against the device checksums of the staged bytes (taken on the D2H stream
+    // right before the copy). GCK_FAULT_FLIP=<i> corrupts one landed byte first (test hook).
+    gck_status verify_step(uint32_t i) {
+        const uint64_t lo = this->lo[i - 1], pe = hi[i - 1] - lo;
+        if (fault_flip == i) reinterpret_cast<uint8_t *>(h_master + lo)[pe * 2] ^= 0x10u;
+        if (!verify) return GCK_OK;
+        return verify_sections(i, nullptr);
     }
 
     // a5, streaming (GCK_REPLAY_STREAM): as soon as session step i+1 has drained (part i+1 at
@@ -544,11 +556,22 @@ struct gck_ctx {
                 cudaError_t e = cudaEventSynchronize(done[K - 1]);
                 if (e != cudaSuccess) st = GCK_E_ABORTED;
             }
-            // a slice that never drained voids the session (GCK_E_INCOMPLETE); drain verification
+            // a slice that never drained voids the session (GCK_E_INCOMPLETE); drain verification.
+            // The batch host replay reads every stale part and every gradient slice exactly once, so
+            // it takes their checksums itself (ReplayChecksums: no extra pass over host DRAM); only
+            // the last part, which no update touches, is summed separately. Other modes verify
+            // before they use the bytes.
+            const bool fold = verify && !replayed && K >= 2 && cfg.replay_mode == GCK_REPLAY_HOST;
             if (st == GCK_OK && !replayed) {
                 const auto v0 = std::chrono::steady_clock::now();
                 for (uint32_t i = 1; i <= K && st == GCK_OK; ++i) st = check_step(i);
-                for (uint32_t i = 1; i <= K && st == GCK_OK; ++i) st = verify_step(i);
+                if (fold) {
+                    for (uint32_t i = 1; i <= K; ++i)
+                        if (fault_flip == i) reinterpret_cast<uint8_t *>(h_master + lo[i - 1])[(hi[i - 1] - lo[i - 1]) * 2] ^= 0x10u;
+                    if (st == GCK_OK) st = verify_sections(K, nullptr);  // the last part: 3 state sections
+                } else {
+                    for (uint32_t i = 1; i <= K && st == GCK_OK; ++i) st = verify_step(i);
+                }
                 stats.last_verify_ms =
                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - v0).count();
             }
@@ -557,11 +580,16 @@ struct gck_ctx {
                 const uint16_t *gl[GCK_K_LIMIT];
                 for (uint32_t i = 0; i < K; ++i) gl[i] = glog[i];
                 const auto r0 = std::chrono::steady_clock::now();
-                if (cfg.replay_mode == GCK_REPLAY_GPU)
+                if (cfg.replay_mode == GCK_REPLAY_GPU) {
                     st = replay_on_gpu();
-                else
+                } else {
+                    gck::ReplayChecksums sums;
+                    std::memset(&sums, 0, sizeof(sums));
                     st = gck::replay_host_impl(recs, K, lo, hi, h_master, h_m, h_v, gl, cfg.replay_threads,
-                                               &replay_threads_used, numa >= 0 ? &numa_cpus : nullptr);
+                                               &replay_threads_used, numa >= 0 ? &numa_cpus : nullptr,
+                                               fold ? &sums : nullptr);
+                    for (uint32_t i = 1; fold && i < K && st == GCK_OK; ++i) st = verify_sections(i, &sums);
+                }
                 replay_compute_ms =
                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - r0).count();
                 replayed = (st == GCK_OK);

@@ -106,10 +106,19 @@ gck_status load_checkpoint_impl(const char *path, float *const dst[3], uint64_t 
 gck_status load_range_impl(const char *path, uint64_t offset, uint64_t count, float *const dst[3], int threads,
                            gck_file_header *hdr_out, std::string *err);
 
-// Host replay (replay_host.cpp).
+// Drain verification folded into the batch replay: the checksums (checksum_host's definition) of the
+// bytes the replay reads, taken before it overwrites them — session step s = part s (0-based) state
+// sections [lo_s, hi_s) of master / m / v (sections 0..2) and gradient slice s (section 3) — so the
+// verification costs no extra pass over host DRAM. Sums are mod 2^64 and order-independent.
+struct ReplayChecksums {
+    uint64_t a[GCK_K_LIMIT][4], b[GCK_K_LIMIT][4];
+};
+
+// Host replay (replay_host.cpp). sums: optional, see ReplayChecksums (every stale part's state and
+// every gradient slice is read exactly once by the batch replay, skipped records included).
 gck_status replay_host_impl(const gck_step_record *recs, uint32_t K, const uint64_t *lo, const uint64_t *hi,
                             float *p, float *m, float *v, const uint16_t *const *glog, int threads,
-                            int *threads_used, const cpu_set_t *cpus = nullptr);
+                            int *threads_used, const cpu_set_t *cpus = nullptr, ReplayChecksums *sums = nullptr);
 int default_threads();
 // Drain verification (replay_host.cpp): A = sum w_i, B = sum (i+1) w_i (mod 2^64) over the
 // little-endian 32-bit words of [p, p+bytes), a partial last word zero-padded.

@@ -343,7 +343,7 @@ __global__ void __launch_bounds__((kCW + 2) * 32, kMinBlocks) fused_adamw_pack_t
 // is not written (the pack warp still bulk-stores the pre-update bytes from it).
 constexpr int tmast_smem(int stages, int outs, int tile) { return (stages + outs) * tile * 14 + 2 * (stages + outs) * 8; }
 
-template <bool PACK, int kStages, int kOut, int kCW, int kTile>
+template <bool PACK, int kStages, int kOut, int kCW, int kTile, bool kUnitFast = false>
 __global__ void __launch_bounds__((kCW + 3) * 32, 1) fused_adamw_pack_tmast_kernel(const FusedArgs a) {
     // warps 0..kCW-1 consume; warp kCW loads; warp kCW+1 packs (session); warp kCW+2 stores
     constexpr int kThreads = kCW * 32;
@@ -490,7 +490,10 @@ __global__ void __launch_bounds__((kCW + 3) * 32, 1) fused_adamw_pack_tmast_kern
                   v[4] = {vq[q].x, vq[q].y, vq[q].z, vq[q].w};
             if (!skip) {
                 const uint32_t gb[4] = {gq[q].x & 0xFFFFu, gq[q].x >> 16, gq[q].y & 0xFFFFu, gq[q].y >> 16};
-                adamw_group_fast(p, m, v, gb, r);
+                if (kUnitFast)  // gs == 1 and the record's ranges checked on the host: min/max guard
+                    adamw_group_mm<4, true, true>(p, m, v, gb, r);
+                else
+                    adamw_group_fast(p, m, v, gb, r);
                 op[c + q * kThreads] = make_float4(p[0], p[1], p[2], p[3]);
                 om[c + q * kThreads] = make_float4(m[0], m[1], m[2], m[3]);
                 ov[c + q * kThreads] = make_float4(v[0], v[1], v[2], v[3]);
@@ -797,6 +800,25 @@ int launch_tmast(const FusedArgs &a, bool pack, cudaStream_t s, int num_sms) {
     const uint64_t cap = (uint64_t)(num_sms > 0 ? num_sms : 148);
     const unsigned grid = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, cap));
     const unsigned block = (CW + 3) * 32;
+    const gck_step_record &r = a.rec;  // host mirror of to_recf's range test + unit grad_scale
+    const bool unit_fast = r.gs == 1.0f && r.bc1 >= 9.5367431640625e-07f && r.bc1 <= 1.0f &&
+                           r.bc2 >= 9.5367431640625e-07f && r.bc2 <= 1.0f && r.eps >= 0.0f && r.eps <= 1.0f &&
+                           !(getenv("GCK_FUSED_GUARD") && getenv("GCK_FUSED_GUARD")[0] == 'g');
+    if (unit_fast && S == 3 && O == 3 && CW == 16) {
+        static std::atomic<uint64_t> attr2{0};
+        if (!(attr2.load() & bit)) {
+            cudaFuncSetAttribute(fused_adamw_pack_tmast_kernel<true, S, O, CW, TL, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, tmast_smem(S, O, TL));
+            cudaFuncSetAttribute(fused_adamw_pack_tmast_kernel<false, S, O, CW, TL, true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, tmast_smem(S, O, TL));
+            attr2.fetch_or(bit);
+        }
+        if (pack)
+            fused_adamw_pack_tmast_kernel<true, S, O, CW, TL, true><<<grid, block, tmast_smem(S, O, TL), s>>>(a);
+        else
+            fused_adamw_pack_tmast_kernel<false, S, O, CW, TL, true><<<grid, block, tmast_smem(S, O, TL), s>>>(a);
+        return (int)cudaGetLastError();
+    }
     if (pack)
         fused_adamw_pack_tmast_kernel<true, S, O, CW, TL><<<grid, block, tmast_smem(S, O, TL), s>>>(a);
     else

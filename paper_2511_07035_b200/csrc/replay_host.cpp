@@ -20,6 +20,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstring>
+#include <mutex>
 #include <thread>
 #include <vector>
 
@@ -139,7 +140,7 @@ void checksum_host(const void *p, uint64_t bytes, uint64_t *A, uint64_t *B, int 
 
 gck_status replay_host_impl(const gck_step_record *recs, uint32_t K, const uint64_t *lo, const uint64_t *hi,
                             float *p, float *m, float *v, const uint16_t *const *glog, int threads,
-                            int *threads_used, const cpu_set_t *cpus) {
+                            int *threads_used, const cpu_set_t *cpus, ReplayChecksums *sums) {
     if (K <= 1) {
         if (threads_used) *threads_used = 0;
         return GCK_OK;
@@ -157,6 +158,7 @@ gck_status replay_host_impl(const gck_step_record *recs, uint32_t K, const uint6
     threads = (int)std::min<uint64_t>((uint64_t)threads, std::max<uint64_t>(1, tasks.size()));
     if (threads_used) *threads_used = threads;
     std::atomic<uint64_t> next{0};
+    std::mutex sums_mu;
     auto worker = [&]() {
         if (cpus) pthread_setaffinity_np(pthread_self(), sizeof(cpu_set_t), cpus);  // NUMA-local
         const unsigned saved_csr = _mm_getcsr();
@@ -165,11 +167,39 @@ gck_status replay_host_impl(const gck_step_record *recs, uint32_t K, const uint6
             const uint64_t t = next.fetch_add(1, std::memory_order_relaxed);
             if (t >= tasks.size()) break;
             const Task &tk = tasks[t];
+            uint64_t sa[3] = {0, 0, 0}, sb[3] = {0, 0, 0}, ga[GCK_K_LIMIT] = {}, gb[GCK_K_LIMIT] = {};
             for (uint64_t b0 = tk.a; b0 < tk.b; b0 += kBlock) {
                 const int cnt = (int)std::min<uint64_t>(kBlock, tk.b - b0);
+                if (sums) {  // the block's landed bytes, before the first update overwrites them (in L1)
+                    const float *sec[3] = {p + b0, m + b0, v + b0};
+                    const uint64_t w0 = b0 - lo[tk.j];  // word index inside the part's sections
+                    for (int k = 0; k < 3; ++k) {
+                        uint64_t a = 0, b = 0;
+                        sum_words(reinterpret_cast<const uint32_t *>(sec[k]), (uint32_t)cnt, &a, &b);
+                        sa[k] += a;
+                        sb[k] += b + w0 * a;
+                    }
+                    for (uint32_t i = tk.j; i + 1 < K; ++i) {  // slice i's words [b0/2, (b0+cnt)/2)
+                        uint64_t a = 0, b = 0;
+                        sum_words(reinterpret_cast<const uint32_t *>(glog[i] + b0), (uint32_t)cnt / 2, &a, &b);
+                        ga[i] += a;
+                        gb[i] += b + (b0 / 2) * a;
+                    }
+                }
                 for (uint32_t i = tk.j; i + 1 < K; ++i) {  // updates t0+j+1 .. t0+K-1 (1-based parts)
                     if (recs[i].skip) continue;
                     update_block(p + b0, m + b0, v + b0, glog[i] + b0, cnt, rr[i]);
+                }
+            }
+            if (sums) {
+                std::lock_guard<std::mutex> lk(sums_mu);
+                for (int k = 0; k < 3; ++k) {
+                    sums->a[tk.j][k] += sa[k];
+                    sums->b[tk.j][k] += sb[k];
+                }
+                for (uint32_t i = tk.j; i + 1 < K; ++i) {
+                    sums->a[i][3] += ga[i];
+                    sums->b[i][3] += gb[i];
                 }
             }
         }
