@@ -99,6 +99,9 @@ def parse():
     ap.add_argument("--verify-drain", type=int, default=1,
                     help="1 (library default): checksum every drained slice on the device and the host "
                          "(a3 verification); 0: off")
+    ap.add_argument("--force-collectives", action="store_true",
+                    help="run the NCCL reduce-scatter / all-gather path even at N = 1 (a process group of one; "
+                         "needs the torchrun environment or MASTER_ADDR/MASTER_PORT)")
     ap.add_argument("--step-log", default="",
                     help="write one JSON line per timed training step to this path (rank-suffixed when N > 1)")
     return ap.parse_args()
@@ -249,7 +252,8 @@ def config_dict(args, world):
             "verify_drain": bool(args.verify_drain),
             "scheme": args.scheme, "replay_mode": args.replay_mode,
             "dist_backend": args.dist_backend if world > 1 else None,
-            "rs_bucket_mb": args.rs_bucket_mb if world > 1 and args.dist_backend == "nccl" else None,
+            "rs_bucket_mb": args.rs_bucket_mb if (world > 1 or getattr(args, "force_collectives", False))
+            and args.dist_backend == "nccl" else None,
             "parallelism": f"zero1-dp{world}",
             "l2": f"inputs larger than L2 ({12 * args.n / 1e9:.2f} GB fp32 state + {2 * args.n / 1e9:.2f} GB "
                   f"gradient per step per rank)" if args.n * 14 > 126e6 else
@@ -319,8 +323,10 @@ def main():
         raise SystemExit("bench.py needs a CUDA device (there is no CPU fallback)")
     local = local % torch.cuda.device_count()   # gloo smoke runs may put several ranks on one GPU
     torch.cuda.set_device(local)
-    coll = world > 1 and args.dist_backend == "nccl"   # the harness's NCCL reduce-scatter / all-gather
-    if world > 1:
+    # the harness's NCCL reduce-scatter / all-gather (--force-collectives: also at N = 1, a process
+    # group of one, so the bucketed-RS code path and NCCL's init run on a one-GPU box)
+    coll = (world > 1 or args.force_collectives) and args.dist_backend == "nccl"
+    if world > 1 or coll:
         if args.dist_backend == "nccl":
             # NCCL's INFO lines (transport, NVLS) stay on, on stderr (stdout carries the JSON line)
             os.environ.setdefault("NCCL_DEBUG", "INFO")
@@ -723,7 +729,7 @@ def main():
     ctx.close()
     if rank == 0:
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if world > 1 or coll:
         dist.barrier()
         dist.destroy_process_group()
 

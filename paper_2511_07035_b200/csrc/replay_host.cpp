@@ -98,7 +98,7 @@ int default_threads() {
 void checksum_host(const void *p, uint64_t bytes, uint64_t *A, uint64_t *B, int threads, const cpu_set_t *cpus) {
     const uint8_t *src = static_cast<const uint8_t *>(p);
     const uint64_t nw = bytes >> 2;
-    constexpr uint64_t kChunk = 1ull << 24;  // words per task (64 MiB)
+    constexpr uint64_t kChunk = 1ull << 20;  // words per task (4 MiB: enough tasks for every thread)
     const uint64_t ntask = (nw + kChunk - 1) / kChunk;
     std::vector<uint64_t> pa(ntask, 0), pb(ntask, 0);
     std::atomic<uint64_t> next{0};

@@ -18,7 +18,8 @@ for staging in ("ring", "direct"):
     G.h_generate(1, p, 3, 0, 0, 0)
     G.h_generate(2, m, 3)
     G.h_generate(3, v, 3)
-    ctx = G.GoCkpt(p, m, v, out, k_min=K, k_max=K, eager_replay=False, staging=staging)
+    ctx = G.GoCkpt(p, m, v, out, k_min=K, k_max=K, eager_replay=False, staging=staging,
+                   verify_drain=os.environ.get("GCK_SANITIZE_VERIFY", "1") != "0")
     s = 0
     for _ in range(2):
         s += 1

@@ -83,3 +83,27 @@ def test_resolve_shards():
         a = type("A", (), dict(model=model, shard_of=W, n=0, tokens=0))()
         bench.resolve(a)
         assert a.n == want and a.tokens > 0 and a.W == W
+
+
+def test_rs_buckets_cover_the_shard():
+    """The ZeRO-1 reduce-scatter buckets (N > 1 with NCCL): contiguous, in order, covering [0, n) of the
+    rank's shard, each input (world x count bf16) at most the bucket size, counts 512-aligned but the last."""
+    sys.path.insert(0, ROOT)
+    from paper_2511_07035_b200.harness import rs_buckets
+    for n, world, mb in [(842_301_952, 8, 512), (3_253_966_336, 4, 512), (124_439_808, 2, 64), (1000, 8, 512)]:
+        b = rs_buckets(n, world, mb << 20)
+        assert b[0][0] == 0 and sum(c for _, c in b) == n
+        assert all(o2 == o1 + c1 for (o1, c1), (o2, _) in zip(b, b[1:]))
+        assert all(2 * world * c <= max(mb << 20, 2 * world * 512) for _, c in b)
+        assert all(c % 512 == 0 for _, c in b[:-1])
+
+
+def test_standin_flops_match_the_model_shapes():
+    """The stand-in's analytic FLOPs (config fb_tflop_per_step, both arms) = 3 x 2 MKN over its GEMMs;
+    ~6 x params x tokens for the matmul weights plus attention."""
+    sys.path.insert(0, ROOT)
+    from paper_2511_07035_b200.harness import MODELS, standin_flops
+    for model, tokens in [("gpt2-small", 16384), ("llama2-7b", 8192), ("llama2-13b", 2048)]:
+        f = standin_flops(model, tokens)
+        params = MODELS[model][0]
+        assert 5.5 * params * tokens < f < 9.0 * params * tokens, (model, f / (params * tokens))

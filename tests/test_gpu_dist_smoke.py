@@ -92,3 +92,18 @@ def test_flat_1m_line_and_step_log(tmp_path):
     sess = [r_ for r_ in recs if r_["part"]]
     assert all(r_["d2h_bytes"] > 0 and r_["fused_ms"] > 0 and r_["slot"] in (0, 1) for r_ in sess)
     assert sum(r_["d2h_bytes"] for r_ in recs[:10]) == d["d2h"]["bytes_per_session"]
+
+
+def test_nccl_bucketed_reduce_scatter_path_on_one_gpu():
+    """The N > 1 NCCL path of the harness (per-bucket async reduce-scatter during the split backward,
+    the param all-gather, NCCL init with INFO lines on stderr) as a process group of one: the only
+    NCCL run a one-GPU box allows (NCCL refuses two ranks on one device)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1", "--master-addr",
+           "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "bench.py"), "--gpus", "1",
+           "--force-collectives", "--rs-bucket-mb", "64", "--steps", "2", "--warmup", "3", "--interval", "10",
+           "--K", "4", "--no-e2e", "--no-cpu-baseline"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    d = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")][0]
+    assert d["config"]["rs_bucket_mb"] == 64 and d["value"] > 0 and d["stall"]["session_steps_measured"] == 8
+    assert "NCCL INFO" in r.stderr
