@@ -309,6 +309,11 @@ def main():
     if args.impl == "reference":
         return run_reference(args)
     assert args.warmup >= 3, "W >= 3 warm-up steps"
+    if args.dist_backend == "nccl" and (world > 1 or args.force_collectives):
+        # NCCL's INFO lines (transport, NVLS) stay on, on stderr (stdout carries the JSON line); set
+        # before torch loads NCCL, which reads them once
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -328,9 +333,6 @@ def main():
     coll = (world > 1 or args.force_collectives) and args.dist_backend == "nccl"
     if world > 1 or coll:
         if args.dist_backend == "nccl":
-            # NCCL's INFO lines (transport, NVLS) stay on, on stderr (stdout carries the JSON line)
-            os.environ.setdefault("NCCL_DEBUG", "INFO")
-            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group("gloo")

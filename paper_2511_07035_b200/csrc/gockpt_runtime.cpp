@@ -259,6 +259,7 @@ struct gck_ctx {
     gck_status worker_status = GCK_OK;
     double replay_ms = 0;          // worker wall time: waits for the drains + replay
     double replay_compute_ms = 0;  // the host replay itself
+    double verify_ms = 0;          // completeness check + drain verification outside the replay pass
     int replay_threads_used = 0;
 
     // streaming replay (GCK_REPLAY_STREAM): slices land in B recycled buffers of slice_elems
@@ -294,7 +295,10 @@ struct gck_ctx {
     bool verify = false;
     unsigned long long *dsum = nullptr;  // device: [GCK_K_LIMIT][4 sections][A, B] of the staged bytes
     unsigned long long *hsum = nullptr;  // pinned host mirror, copied on the D2H stream before the drain
-    uint64_t state_mask = 0, grad_mask = 0;  // session steps whose state part / gradient slice drained
+    // session steps whose state part / gradient slice drained: set by the submitting thread, read by the
+    // streaming worker while later bits are still being set (atomics; relaxed — the worker reads bit i
+    // only after the step was published under mu)
+    std::atomic<uint64_t> state_mask{0}, grad_mask{0};
     uint32_t fault_drop = 0, fault_flip = 0;  // GCK_FAULT_DROP_SLICE / GCK_FAULT_FLIP (read at begin)
     std::string worker_error;                 // why the worker failed (set before worker_done)
 
@@ -333,9 +337,10 @@ struct gck_ctx {
     // mu) and only read here, by the worker after that publication.
     gck_status check_step(uint32_t i) {
         const uint64_t bit = 1ull << (i - 1);
-        if ((state_mask & bit) && (i == K || (grad_mask & bit))) return GCK_OK;
+        const uint64_t sm = state_mask.load(std::memory_order_relaxed), gm = grad_mask.load(std::memory_order_relaxed);
+        if ((sm & bit) && (i == K || (gm & bit))) return GCK_OK;
         worker_error = "session step " + std::to_string(i) +
-                       (!(state_mask & bit) ? " (state part)" : " (gradient slice)") +
+                       (!(sm & bit) ? " (state part)" : " (gradient slice)") +
                        " never drained: the checkpoint is incomplete and discarded";
         return GCK_E_INCOMPLETE;
     }
@@ -572,7 +577,7 @@ struct gck_ctx {
                 } else {
                     for (uint32_t i = 1; i <= K && st == GCK_OK; ++i) st = verify_step(i);
                 }
-                stats.last_verify_ms =
+                verify_ms =
                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - v0).count();
             }
             // replay-on-restore: the stale parts stay as captured; the load replays them
@@ -647,6 +652,7 @@ struct gck_ctx {
         stats.last_session_stall_ms = stall;
         stats.last_session_d2h_ms = d2h_ms;
         stats.last_replay_ms = replay_compute_ms;
+        stats.last_verify_ms = verify_ms;
         stats.last_worker_ms = replay_ms;
         stats.replay_threads = replay_threads_used;
     }
@@ -1021,7 +1027,7 @@ static cudaError_t enqueue_state_copy(gck_ctx *c, uint32_t i) {
         c->stats.d2h_bytes += 3 * pe * 4;
         c->stats.last_session_d2h_bytes += 3 * pe * 4;
         c->step_bytes[i - 1] += 3 * pe * 4;
-        c->state_mask |= 1ull << (i - 1);
+        c->state_mask.fetch_or(1ull << (i - 1), std::memory_order_relaxed);
     } else if (c->cfg.timing) {
         cudaEventRecord(c->ev_d0[i - 1], c->d2h);
         cudaEventRecord(c->ev_d1[i - 1], c->d2h);
@@ -1090,7 +1096,8 @@ gck_status gck_begin_checkpoint(gck_ctx *c, uint64_t t0, uint32_t K) {
     }
     if (off > c->glog_elems_cap) return c->fail(GCK_E_INVALID, "gradient log capacity exceeded");
     c->stats.last_session_d2h_bytes = 0;
-    c->state_mask = c->grad_mask = 0;
+    c->state_mask.store(0);
+    c->grad_mask.store(0);
     std::memset(c->step_bytes, 0, sizeof(c->step_bytes));
     c->worker_error.clear();
     c->K = K;  // the drain/verify paths below read K
@@ -1114,6 +1121,7 @@ gck_status gck_begin_checkpoint(gck_ctx *c, uint64_t t0, uint32_t K) {
     c->worker_status = GCK_OK;
     c->replay_ms = 0;
     c->replay_compute_ms = 0;
+    c->verify_ms = 0;
     c->state = State::ACTIVE;
     if (c->stream_mode) {  // the streaming worker follows the drains from the first one on
         c->join_worker();
@@ -1202,8 +1210,8 @@ static gck_status enqueue_drain(gck_ctx *c, uint32_t i, const SlotLayout &L, cha
     c->stats.d2h_bytes += tot;
     c->stats.last_session_d2h_bytes += tot;
     c->step_bytes[i - 1] += tot;
-    c->state_mask |= 1ull << (i - 1);
-    if (ghi) c->grad_mask |= 1ull << (i - 1);
+    c->state_mask.fetch_or(1ull << (i - 1), std::memory_order_relaxed);
+    if (ghi) c->grad_mask.fetch_or(1ull << (i - 1), std::memory_order_relaxed);
     return GCK_OK;
 }
 
@@ -1267,7 +1275,7 @@ static gck_status submit_direct(gck_ctx *c, uint32_t i, const gck_step_args *a, 
             c->stats.d2h_bytes += ghi * 2;
             c->stats.last_session_d2h_bytes += ghi * 2;
             c->step_bytes[i - 1] += ghi * 2;
-            c->grad_mask |= 1ull << (i - 1);
+            c->grad_mask.fetch_or(1ull << (i - 1), std::memory_order_relaxed);
         }
     }
     // a4 (direct): the update may not overwrite part i before its state copy has been taken;

@@ -57,14 +57,31 @@ __attribute__((target_clones("avx512f", "avx2", "default"))) void update_block(
     }
 }
 
-// Partial checksum of cnt 32-bit words with local indices 0..cnt-1 (see checksum_host).
+// Partial checksum of cnt 32-bit words with local indices 0..cnt-1 (see checksum_host):
+// A = sum w_k, B = sum (k+1) w_k, mod 2^64. Computed without multiplies in the loop: 8 interleaved
+// Fletcher lanes (lane l takes words l, l+8, ...: a_l += w; b_l += a_l, so after M words
+// b_l = sum_m (M - m) w_{l+8m}), combined exactly at the end:
+// B = sum_l [(l+1) a_l + 8 (M a_l - b_l)]  (all mod 2^64), plus the scalar tail.
 __attribute__((target_clones("avx512f", "avx2", "default"))) void sum_words(const uint32_t *__restrict w,
                                                                          uint32_t cnt, uint64_t *a, uint64_t *b) {
+    constexpr int L = 8;
+    uint64_t la[L] = {0}, lb[L] = {0};
+    const uint32_t M = cnt / L;
+    for (uint32_t mm = 0; mm < M; ++mm) {
+        const uint32_t *q = w + (uint64_t)mm * L;
+        for (int l = 0; l < L; ++l) {
+            la[l] += q[l];
+            lb[l] += la[l];
+        }
+    }
     uint64_t A = 0, B = 0;
-    for (uint32_t k = 0; k < cnt; ++k) {
-        const uint64_t x = w[k];
-        A += x;
-        B += (uint64_t)(k + 1) * x;
+    for (int l = 0; l < L; ++l) {
+        A += la[l];
+        B += (uint64_t)(l + 1) * la[l] + (uint64_t)L * ((uint64_t)M * la[l] - lb[l]);
+    }
+    for (uint32_t k = M * L; k < cnt; ++k) {
+        A += w[k];
+        B += (uint64_t)(k + 1) * w[k];
     }
     *a = A;
     *b = B;
@@ -179,14 +196,14 @@ gck_status replay_host_impl(const gck_step_record *recs, uint32_t K, const uint6
                         sa[k] += a;
                         sb[k] += b + w0 * a;
                     }
-                    for (uint32_t i = tk.j; i + 1 < K; ++i) {  // slice i's words [b0/2, (b0+cnt)/2)
+                }
+                for (uint32_t i = tk.j; i + 1 < K; ++i) {  // updates t0+j+1 .. t0+K-1 (1-based parts)
+                    if (sums) {  // slice i's words [b0/2, (b0+cnt)/2), right before the update reads them
                         uint64_t a = 0, b = 0;
                         sum_words(reinterpret_cast<const uint32_t *>(glog[i] + b0), (uint32_t)cnt / 2, &a, &b);
                         ga[i] += a;
                         gb[i] += b + (b0 / 2) * a;
                     }
-                }
-                for (uint32_t i = tk.j; i + 1 < K; ++i) {  // updates t0+j+1 .. t0+K-1 (1-based parts)
                     if (recs[i].skip) continue;
                     update_block(p + b0, m + b0, v + b0, glog[i] + b0, cnt, rr[i]);
                 }

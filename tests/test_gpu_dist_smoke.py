@@ -106,4 +106,4 @@ def test_nccl_bucketed_reduce_scatter_path_on_one_gpu():
     assert r.returncode == 0, r.stderr[-3000:]
     d = [json.loads(l) for l in r.stdout.splitlines() if l.startswith("{")][0]
     assert d["config"]["rs_bucket_mb"] == 64 and d["value"] > 0 and d["stall"]["session_steps_measured"] == 8
-    assert "NCCL INFO" in r.stderr
+    assert "NCCL INFO" in r.stderr + r.stdout, (r.stderr[-2000:], r.stdout[-2000:])
