@@ -312,7 +312,8 @@ def main():
     if args.dist_backend == "nccl" and (world > 1 or args.force_collectives):
         # NCCL's INFO lines (transport, NVLS) stay on, on stderr (stdout carries the JSON line); set
         # before torch loads NCCL, which reads them once
-        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        if os.environ.get("NCCL_DEBUG", "VERSION").upper() in ("VERSION", ""):  # the image sets VERSION
+            os.environ["NCCL_DEBUG"] = "INFO"
         os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
     import numpy as np
     import torch

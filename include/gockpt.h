@@ -292,7 +292,9 @@ gck_status gck_finalize(gck_ctx *ctx, gck_checkpoint *out);
 /* Non-blocking finalize: GCK_E_BUSY while drains/replay are still running. */
 gck_status gck_finalize_poll(gck_ctx *ctx, gck_checkpoint *out);
 
-/* Return the checkpoint memory to the library; the next session may begin. */
+/* Return the checkpoint memory to the library; the next session may begin. Also the way out of a
+ * voided session (ABORTED / INCOMPLETE / CORRUPT): release then waits for the library's threads and its
+ * D2H stream, so no copy of the voided session can still land in the pinned arena afterwards. */
 gck_status gck_release(gck_ctx *ctx);
 
 /* ---- references and variants -------------------------------------------- */
@@ -470,7 +472,8 @@ gck_status gck_persist_wait(gck_ctx *ctx, gck_persist_stats *out);
  * A version-2 file's gradient slices go up to temporary device memory and the replay kernel
  * brings the stale parts to S(T) in place on the device tensors before the bf16 cast
  * (replay-on-restore: HBM-speed reconstruction, no host arithmetic). A version-2 file's K may
- * exceed the context's k_max. Errors: PROTOCOL, INVALID (n mismatch), IO, CORRUPT, NOMEM, CUDA. */
+ * exceed the context's k_max. Before it touches the arena it joins the library's threads and waits
+ * for its D2H stream. Errors: PROTOCOL, INVALID (n mismatch), IO, CORRUPT, NOMEM, CUDA. */
 gck_status gck_restore(gck_ctx *ctx, const char *path, void *stream, gck_file_header *out);
 
 /* ---- NEXT-4: analytic model (§3.1; §4.2.3) and K selection ------ */
