@@ -149,3 +149,26 @@ def test_planted_out_of_range_lanes(G, gs_big):
     traj, parts = run_session(G, state, grads, recs, sargs, t0, K)
     assert guard_failures(traj) > 100
     assert replay_guard_failures(traj, parts, K) > 100
+
+
+@pytest.mark.parametrize("K,skips", [(4, (3,)), (8, (7,)), (8, (5, 6, 7)), (8, (1, 2)), (6, (1, 3, 5)),
+                                     (8, (2, 3, 4, 5, 6, 7))])
+def test_replay_kernel_compaction_with_skipped_updates(G, K, skips):
+    """The replay kernel keeps only the non-skipped StepRecords (compacted on the host; part j needs the
+    compacted records from first[j] on). Skipped updates at the end of the session leave whole stale
+    parts with nothing pending (the kernel must not load or store them), skips at the start shift every
+    part's first record. The GPU replay (and the host replay) == the synchronous snapshot == oracle O1.
+    skips are session steps i (training step t0 + i); the bias-correction count does not advance."""
+    n, t0, seed = (1 << 18) + 2048 * 5 + 64, 30, 13
+    state = gi.warm_state(seed, n)
+    grads = [gi.grad_bits(seed, t0 + i, n) for i in range(1, K + 1)]
+    recs, sargs, t = [], [], t0
+    for i in range(1, K + 1):
+        sk = i in skips
+        if not sk:
+            t += 1
+        gs = 0.5 if i % 3 == 0 else 1.0
+        recs.append(oracle.make_step_record(t=t, lr=1e-3, grad_scale=gs, skip=sk, **HP))
+        sargs.append(dict(step=t0 + i, adam_t=max(t, 1), lr=1e-3, grad_scale=gs, skip=sk))
+    traj, parts = run_session(G, state, grads, recs, sargs, t0, K, A=64)
+    assert len(parts) == K

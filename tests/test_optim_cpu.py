@@ -53,3 +53,95 @@ def test_prune_keeps_newest_and_pointed_to(tmp_path):
     assert all(f"ckpt_{st}.rank1.bin" in left for st in (3, 15, 27, 39, 51))   # other ranks' files untouched
     assert len(gone) == 5
     assert prune_checkpoints(d, 0, keep=0) == []
+
+
+# ---------------------------------------------------------------- the optimizer face at world 2 (gloo)
+class _FakeCtx:
+    """Stands in for GoCkpt (no GPU here): records the calls, 'persists' a small file, and can void a
+    chosen session the way the library does (finalize raises GCK_E_CORRUPT)."""
+
+    def __init__(self, *a, fail_t=None, rank=0, **kw):
+        self.fail_t, self.rank, self.sess, self.held = fail_t, rank, None, None
+
+    def begin_checkpoint(self, t0, K):
+        self.sess = (t0, K)
+
+    def stats(self):
+        return {"last_session_k": self.sess[1] if self.sess else 0}
+
+    def submit(self, part, step, adam_t, lr, grad, gs=1.0, skip=False, stream=None):
+        return 0
+
+    def finalize(self, block=True):
+        from paper_2511_07035_b200._lib import E_CORRUPT, GckError
+        t0, K = self.sess
+        if t0 + K - 1 == self.fail_t:
+            raise GckError(E_CORRUPT, "drain verification: injected")
+        from types import SimpleNamespace
+        self.held = t0 + K - 1
+        return SimpleNamespace(step=t0 + K - 1)
+
+    def persist_begin(self, path, rank, world, meta_json=None):
+        with open(path, "w") as fh:
+            fh.write("x")
+        d = os.path.dirname(path)
+        with open(os.path.join(d, f"LATEST.rank{rank}"), "w") as fh:
+            fh.write(os.path.basename(path) + "\n")
+
+    def persist_wait(self):
+        return {}
+
+    def release(self):
+        self.held = None
+
+    def close(self):
+        pass
+
+
+def _opt_worker(rank, world, port, d, fail_rank, fail_t, q):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2511_07035_b200.optim as O
+        O.GoCkpt = lambda *a, **kw: _FakeCtx(fail_t=fail_t if rank == fail_rank else None, rank=rank)
+        opt = O.CheckpointedAdamW(None, None, None, K=4, persist_dir=d, rank=rank, world=world, keep=2)
+        manifests = []
+        for s in range(1, 61):
+            if s % 12 == 1:
+                opt.save_checkpoint()
+            opt.step(None)
+            if s % 12 == 1 and rank == 0 and os.path.exists(os.path.join(d, "MANIFEST.json")):
+                manifests.append(json.load(open(os.path.join(d, "MANIFEST.json")))["step"])
+        opt.wait()
+        if rank == 0:
+            manifests.append(json.load(open(os.path.join(d, "MANIFEST.json")))["step"])
+        q.put((rank, [f[:2] for f in opt.failures], manifests, sorted(os.listdir(d))))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_global_manifest_lockstep_with_a_voided_rank(tmp_path):
+    """world 2: checkpoints at T = 3, 15, 27, 39, 51; rank 1's T = 27 is voided (CORRUPT). Both ranks
+    reach the global commit at the same steps (no deadlock), the manifest never names 27, it names
+    the newest step every rank made durable, and retention keeps 2 files per rank plus the manifest's."""
+    import socket
+    import torch.multiprocessing as mp
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_opt_worker, args=(r, 2, port, str(tmp_path), 1, 27, q)) for r in range(2)]
+    for p_ in procs:
+        p_.start()
+    res = dict((r, (f, m, ls)) for r, f, m, ls in (q.get(timeout=120) for _ in procs))
+    for p_ in procs:
+        p_.join(timeout=60)
+        assert p_.exitcode == 0
+    assert res[0][0] == [] and res[1][0] == [(27, "GCK_E_CORRUPT")]
+    manifests = res[0][1]
+    assert 27 not in manifests and manifests[-1] == 51
+    assert manifests == sorted(manifests)
+    files = res[0][2]
+    assert "ckpt_51.rank0.bin" in files and "ckpt_51.rank1.bin" in files and "ckpt_3.rank0.bin" not in files
