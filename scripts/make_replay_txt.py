@@ -11,6 +11,8 @@ LEGEND = {
     "r02_replay8.jsonl": "f4/f5/f6 = 4 elements per thread at 4/5/6 CTAs per SM, p = packed, r = kept kernel",
     "r02_replay9.jsonl": "pref = 0 kept kernel, 1 + L2 bulk prefetch of the warp's next group, 2 + the "
                          "gradient two steps ahead (each twice)",
+    "r02_replay10.jsonl": "coalesced = 0 the 8-consecutive-element kernel, 1 the warp-coalesced default "
+                          "(each twice)",
     "r02_replay_final.jsonl": "t = the kept kernel as committed (default), s = the round-1 kernel "
                               "(replay_generic_kernel, GCK_REPLAY_IMPL=s), alternated twice",
 }
@@ -26,7 +28,7 @@ for f, leg in LEGEND.items():
         except ValueError:
             continue
         r = d["r"]
-        tag = str(d.get("impl", d.get("pref", ""))) + (f" minb{d['minb']}" if "minb" in d else "") + (f" T{d['T']}" if "T" in d else "")
+        tag = str(d.get("impl", d.get("pref", d.get("coalesced", "")))) + (f" minb{d['minb']}" if "minb" in d else "") + (f" T{d['T']}" if "T" in d else "")
         lines.append(f"    {tag:9s} n={r['n']:>11,d} K={r['K']:>2d}  {r['us_mean']:8.1f} us  {r['gbs']:7.1f} GB/s  "
                      f"{r['gbs'] / 6555.2:.3f}")
 open("profiles/r02_replay_kernel.txt", "w").write("\n".join(lines) + "\n")
