@@ -68,7 +68,6 @@ int launch_cast_bf16(const float *src, uint16_t *dst, uint64_t n, void *stream, 
 // Drain verification: d_out[2s], d_out[2s+1] = (A, B) checksums of section s (checksum_host's
 // definition), zeroed first; async on stream.
 int launch_checksum(const ZcArgs &a, unsigned long long *d_out, void *stream, int num_sms);
-int launch_flip_byte(void *dev_byte, void *stream);  // test hook: XOR one device byte
 
 // Persistence (persist.cpp).
 // The replay log a version-2 (replay-on-restore) file carries: the session plan, its K

@@ -745,8 +745,6 @@ __global__ void __launch_bounds__(256) checksum_kernel(const ZcArgs a, unsigned 
     }
 }
 
-// Test hook (GCK_FAULT_FLIP): XOR one byte of device memory.
-__global__ void flip_byte_kernel(uint8_t *p) { *p ^= 0x10u; }
 
 // ---- harness-only generator (gockpt_inputs.py) ----
 __device__ __forceinline__ uint64_t mix64(uint64_t z) {
@@ -1023,11 +1021,6 @@ int launch_checksum(const ZcArgs &a, unsigned long long *d_out, void *stream, in
     uint64_t maxv = 1;
     for (int k = 0; k < a.count; ++k) maxv = std::max<uint64_t>(maxv, a.bytes[k] >> 4);
     checksum_kernel<<<grid_for(maxv, 256, num_sms, 4), 256, 0, s>>>(a, d_out);
-    return (int)cudaGetLastError();
-}
-
-int launch_flip_byte(void *dev_byte, void *stream) {
-    flip_byte_kernel<<<1, 1, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<uint8_t *>(dev_byte));
     return (int)cudaGetLastError();
 }
 
