@@ -988,13 +988,19 @@ int launch_replay(const ReplayArgs &a, void *stream, int num_sms) {
     ReplayPlan rp;
     bool unit_gs = false;
     if (replay_plan(a, &rp, &unit_gs)) {
-        const unsigned grid = grid_for(a.n_replay >> 3, 256, num_sms, 8);
+        // 64 CTAs per SM (~5 grid-stride iterations per thread at GPT-2 size): the CTA scheduler then
+        // keeps starting fresh CTAs on every SM while others are still on earlier parts, which mixes
+        // the FP-heavy first parts with the HBM-heavy last parts on each SM (r02_replay11.jsonl: 8 per SM
+        // 644 us, 16: 618, 64: 611 at GPT-2/K=8; K=4 444 -> 408 us; one wave (4): 695 us)
+        const char *w = getenv("GCK_REPLAY_CTAS_PER_SM");  // experiment knob
+        const unsigned grid = grid_for(a.n_replay >> 3, 256, num_sms, w ? (unsigned)atoi(w) : 64);
         bool b256 = (a.n_replay & 255u) == 0;
         for (uint32_t i = 0; i + 1 < a.K; ++i) b256 = b256 && ((a.hi[i] & 255u) == 0);
         const char *ce = getenv("GCK_REPLAY_COALESCED");  // "0": the 8-consecutive-element form
         if (b256 && !(ce && ce[0] == '0')) {
+            const unsigned g2 = grid;
             switch ((unit_gs ? 2 : 0) | (all_fast(rp) ? 1 : 0)) {
-                case 3: replay_coalesced_kernel<true, true><<<grid, 256, 0, s>>>(rp); break;
+                case 3: replay_coalesced_kernel<true, true><<<g2, 256, 0, s>>>(rp); break;
                 case 2: replay_coalesced_kernel<true, false><<<grid, 256, 0, s>>>(rp); break;
                 case 1: replay_coalesced_kernel<false, true><<<grid, 256, 0, s>>>(rp); break;
                 default: replay_coalesced_kernel<false, false><<<grid, 256, 0, s>>>(rp); break;
@@ -1009,7 +1015,7 @@ int launch_replay(const ReplayArgs &a, void *stream, int num_sms) {
         }
         return (int)cudaGetLastError();
     }
-    const unsigned grid = grid_for((a.n_replay + 7) >> 3, 256, num_sms, 8);
+    const unsigned grid = grid_for((a.n_replay + 7) >> 3, 256, num_sms, 64);
     replay_generic_kernel<<<grid, 256, 0, s>>>(a);
     return (int)cudaGetLastError();
 }

@@ -13,6 +13,10 @@ LEGEND = {
                          "gradient two steps ahead (each twice)",
     "r02_replay10.jsonl": "coalesced = 0 the 8-consecutive-element kernel, 1 the warp-coalesced default "
                           "(each twice)",
+    "r02_replay11_grid_a.jsonl": "ctas_per_sm = grid size of the coalesced kernel (grid-stride), twice",
+    "r02_replay11.jsonl": "ctas_per_sm, larger grids (100000 = one group per thread)",
+    "r02_replay12.jsonl": "FINAL: t = the kernel as committed (coalesced, 64 CTAs/SM), s = the round-1 kernel with "
+                          "the same grid; twice",
     "r02_replay_final.jsonl": "t = the kept kernel as committed (default), s = the round-1 kernel "
                               "(replay_generic_kernel, GCK_REPLAY_IMPL=s), alternated twice",
 }
@@ -28,7 +32,7 @@ for f, leg in LEGEND.items():
         except ValueError:
             continue
         r = d["r"]
-        tag = str(d.get("impl", d.get("pref", d.get("coalesced", "")))) + (f" minb{d['minb']}" if "minb" in d else "") + (f" T{d['T']}" if "T" in d else "")
+        tag = str(d.get("impl", d.get("pref", d.get("coalesced", d.get("ctas_per_sm", ""))))) + (f" minb{d['minb']}" if "minb" in d else "") + (f" T{d['T']}" if "T" in d else "")
         lines.append(f"    {tag:9s} n={r['n']:>11,d} K={r['K']:>2d}  {r['us_mean']:8.1f} us  {r['gbs']:7.1f} GB/s  "
                      f"{r['gbs'] / 6555.2:.3f}")
 open("profiles/r02_replay_kernel.txt", "w").write("\n".join(lines) + "\n")
