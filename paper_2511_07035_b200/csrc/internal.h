@@ -123,4 +123,16 @@ int default_threads();
 // little-endian 32-bit words of [p, p+bytes), a partial last word zero-padded.
 void checksum_host(const void *p, uint64_t bytes, uint64_t *A, uint64_t *B, int threads, const cpu_set_t *cpus);
 
+// Keeping DMA destinations out of the CPU caches (replay_host.cpp). The next session's drains
+// DMA-write into the pinned arena; a line a host pass (replay, verification, persist) left in a
+// core's cache turns each such write into a snoop + invalidate (+ write-back): measured on the
+// B200 box, 1 MiB D2H copies into lines the replay threads had touched took 100-230 us instead of
+// 22 us (profiles/r02_small_drain.txt). The host passes therefore write back and drop the lines
+// of the tail of their work that can still be cached: evict_budget() bytes (2 x (all L2s + L3);
+// GCK_EVICT_BYTES overrides, 0 = off), evicted with evict_lines() (clflushopt, else clflush;
+// weakly ordered: evict_fence() once at the end of each thread's pass).
+uint64_t evict_budget();
+void evict_lines(const void *p, uint64_t bytes);
+void evict_fence();
+
 }  // namespace gck

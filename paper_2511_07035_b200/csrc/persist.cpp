@@ -203,7 +203,12 @@ gck_status write_checkpoint_impl(const char *path, const gck_file_header *hdr_in
     std::atomic<uint64_t> next{0};
     std::atomic<bool> failed{false};
     const long fault = fault_after_blocks();
+    // the blocks written last may still be cached when the next session's drains DMA-write the
+    // arena (evict_budget, internal.h): their lines are evicted after the pwrite
+    const uint64_t tail = evict_budget() / kBlock + 1;
+    const uint64_t first_evict = total > tail ? total - tail : 0;
     auto worker = [&]() {
+        bool evicted = false;
         for (;;) {
             const uint64_t j = next.fetch_add(1);
             if (j >= total || failed.load()) break;
@@ -218,6 +223,10 @@ gck_status write_checkpoint_impl(const char *path, const gck_file_header *hdr_in
                 const char *src = reinterpret_cast<const char *>(sec[s]) + off;
                 table[j] = crc32_of(src, len);
                 if (!pwrite_all(fd, src, len, L.sec_off[s] + off)) failed = true;
+                if (j >= first_evict) {
+                    evict_lines(src, len);
+                    evicted = true;
+                }
             } else {
                 const uint64_t gb = j - 3 * L.nblocks;
                 const uint32_t i = gslice[gb];
@@ -225,8 +234,13 @@ gck_status write_checkpoint_impl(const char *path, const gck_file_header *hdr_in
                 const char *src = reinterpret_cast<const char *>(log->glog[i]) + off;
                 gtable[gb] = crc32_of(src, len);
                 if (!pwrite_all(fd, src, len, G.slice_off[i] + off)) failed = true;
+                if (j >= first_evict) {
+                    evict_lines(src, len);
+                    evicted = true;
+                }
             }
         }
+        if (evicted) evict_fence();
     };
     if (threads <= 0) threads = std::min(16, default_threads());
     threads = (int)std::max<uint64_t>(1, std::min<uint64_t>((uint64_t)threads, total));

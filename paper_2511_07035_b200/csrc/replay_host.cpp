@@ -13,12 +13,16 @@
 //
 // Traffic: the batch order streams each stale element once (load p, m, v; K-j updates
 // in L1; store), i.e. 24 B + 2 B per pending step, the minimum for a batch replay.
+#include <cpuid.h>
+#include <immintrin.h>
 #include <pthread.h>
 #include <sched.h>
+#include <unistd.h>
 #include <xmmintrin.h>
 
 #include <algorithm>
 #include <atomic>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <thread>
@@ -99,7 +103,45 @@ void clear_ftz_daz() {
     _mm_setcsr(csr);
 }
 
+bool cpu_has_clflushopt() {
+    unsigned a = 0, b = 0, c = 0, d = 0;
+    return __get_cpuid_count(7, 0, &a, &b, &c, &d) && (b & (1u << 23));
+}
+
+__attribute__((target("clflushopt"))) void flush_opt(const char *a, const char *e) {
+    for (; a < e; a += 64) _mm_clflushopt(const_cast<char *>(a));
+}
+
+void flush_plain(const char *a, const char *e) {
+    for (; a < e; a += 64) _mm_clflush(a);
+}
+
 }  // namespace
+
+uint64_t evict_budget() {
+    static const uint64_t budget = [] {
+        if (const char *e = getenv("GCK_EVICT_BYTES")) return (uint64_t)strtoull(e, nullptr, 10);
+        const long l2 = sysconf(_SC_LEVEL2_CACHE_SIZE), l3 = sysconf(_SC_LEVEL3_CACHE_SIZE);
+        const long cpus = sysconf(_SC_NPROCESSORS_ONLN);
+        uint64_t cached = (l2 > 0 && cpus > 0 ? (uint64_t)l2 * (uint64_t)cpus : 0) + (l3 > 0 ? (uint64_t)l3 : 0);
+        if (cached == 0) cached = 128ull << 20;  // sysconf without cache data: a generous guess
+        return std::max<uint64_t>(2 * cached, 16ull << 20);
+    }();
+    return budget;
+}
+
+void evict_lines(const void *p, uint64_t bytes) {
+    static const bool opt = cpu_has_clflushopt();
+    if (!bytes) return;
+    const char *a = reinterpret_cast<const char *>(reinterpret_cast<uintptr_t>(p) & ~uintptr_t(63));
+    const char *e = static_cast<const char *>(p) + bytes;
+    if (opt)
+        flush_opt(a, e);
+    else
+        flush_plain(a, e);
+}
+
+void evict_fence() { _mm_sfence(); }
 
 int default_threads() {
     cpu_set_t set;
@@ -119,8 +161,12 @@ void checksum_host(const void *p, uint64_t bytes, uint64_t *A, uint64_t *B, int 
     const uint64_t ntask = (nw + kChunk - 1) / kChunk;
     std::vector<uint64_t> pa(ntask, 0), pb(ntask, 0);
     std::atomic<uint64_t> next{0};
+    // the chunks summed last may still be cached when the next drain DMA-writes them: evict them
+    const uint64_t tail = evict_budget() / (kChunk * 4);
+    const uint64_t first_evict = ntask > tail ? ntask - tail : 0;
     auto worker = [&]() {
         if (cpus) pthread_setaffinity_np(pthread_self(), sizeof(cpu_set_t), cpus);
+        bool evicted = false;
         for (;;) {
             const uint64_t t = next.fetch_add(1, std::memory_order_relaxed);
             if (t >= ntask) break;
@@ -129,7 +175,12 @@ void checksum_host(const void *p, uint64_t bytes, uint64_t *A, uint64_t *B, int 
             sum_words(reinterpret_cast<const uint32_t *>(src) + w0, (uint32_t)cnt, &a, &b);
             pa[t] = a;
             pb[t] = b + w0 * a;  // global weights (w0 + k + 1) = local (k + 1) + w0
+            if (t >= first_evict) {
+                evict_lines(src + 4 * w0, 4 * cnt);
+                evicted = true;
+            }
         }
+        if (evicted) evict_fence();
     };
     if (threads <= 0) threads = cpus ? std::max(1, CPU_COUNT(cpus)) : default_threads();
     threads = (int)std::min<uint64_t>((uint64_t)threads, std::max<uint64_t>(1, ntask));
@@ -174,16 +225,28 @@ gck_status replay_host_impl(const gck_step_record *recs, uint32_t K, const uint6
     if (threads <= 0) threads = cpus ? std::max(1, CPU_COUNT(cpus)) : default_threads();
     threads = (int)std::min<uint64_t>((uint64_t)threads, std::max<uint64_t>(1, tasks.size()));
     if (threads_used) *threads_used = threads;
+    // the tasks processed last may still be cached when the next session's drains DMA-write the
+    // same lines (state and gradient log): their blocks are evicted right after their updates
+    uint64_t first_evict = tasks.size();
+    for (uint64_t acc = 0, budget = evict_budget(); first_evict > 0;) {
+        const Task &tk = tasks[first_evict - 1];
+        acc += (tk.b - tk.a) * (12 + 2 * (uint64_t)(K - 1 - tk.j));
+        if (acc > budget) break;
+        --first_evict;
+    }
     std::atomic<uint64_t> next{0};
     std::mutex sums_mu;
     auto worker = [&]() {
         if (cpus) pthread_setaffinity_np(pthread_self(), sizeof(cpu_set_t), cpus);  // NUMA-local
         const unsigned saved_csr = _mm_getcsr();
         clear_ftz_daz();
+        bool evicted = false;
         for (;;) {
             const uint64_t t = next.fetch_add(1, std::memory_order_relaxed);
             if (t >= tasks.size()) break;
             const Task &tk = tasks[t];
+            const bool evict = t >= first_evict;
+            evicted = evicted || evict;
             uint64_t sa[3] = {0, 0, 0}, sb[3] = {0, 0, 0}, ga[GCK_K_LIMIT] = {}, gb[GCK_K_LIMIT] = {};
             for (uint64_t b0 = tk.a; b0 < tk.b; b0 += kBlock) {
                 const int cnt = (int)std::min<uint64_t>(kBlock, tk.b - b0);
@@ -207,6 +270,12 @@ gck_status replay_host_impl(const gck_step_record *recs, uint32_t K, const uint6
                     if (recs[i].skip) continue;
                     update_block(p + b0, m + b0, v + b0, glog[i] + b0, cnt, rr[i]);
                 }
+                if (evict) {
+                    evict_lines(p + b0, 4ull * cnt);
+                    evict_lines(m + b0, 4ull * cnt);
+                    evict_lines(v + b0, 4ull * cnt);
+                    for (uint32_t i = tk.j; i + 1 < K; ++i) evict_lines(glog[i] + b0, 2ull * cnt);
+                }
             }
             if (sums) {
                 std::lock_guard<std::mutex> lk(sums_mu);
@@ -220,6 +289,7 @@ gck_status replay_host_impl(const gck_step_record *recs, uint32_t K, const uint6
                 }
             }
         }
+        if (evicted) evict_fence();
         _mm_setcsr(saved_csr);
     };
     if (threads == 1 && !cpus) {

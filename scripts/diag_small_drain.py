@@ -96,5 +96,53 @@ def main():
     print(json.dumps({"case": "session 16M", **session(n2, K, True)}), flush=True)
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and not os.environ.get("DIAG_TRACE"):
     main()
+
+
+def trace(n=1 << 20, K=4, verify=True):
+    """CUPTI trace (torch.profiler) of one small session: GPU memcpy/kernel durations and the host
+    API durations of the library's calls, to tell device time from host enqueue time."""
+    from torch.profiler import ProfilerActivity, profile
+    hp = dict(beta1=0.9, beta2=0.999, eps=1e-8, weight_decay=0.01)
+    p0, m0, v0 = gi.warm_state(1, n)
+    p, m, v = (torch.from_numpy(x.copy()).cuda() for x in (p0, m0, v0))
+    out = torch.zeros(n, dtype=torch.int16, device="cuda")
+    g = torch.from_numpy(gi.grad_bits(1, 1, n).view(np.int16).copy()).cuda()
+    ctx = G.GoCkpt(p, m, v, out, **hp, k_min=1, k_max=16, part_align=1024, verify_drain=verify)
+    step = 0
+    for s_ in range(4):
+        with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) if s_ == 3 else _Null() as prof:
+            ctx.begin_checkpoint(step, K)
+            for i in range(1, K + 1):
+                step += 1
+                ctx.submit(i, step, step, 1e-3, g)
+            ctx.finalize()
+            torch.cuda.synchronize()
+        print(json.dumps({"session": s_, "steps": ctx.session_steps()}), file=sys.stderr)
+        ctx.release()
+    ctx.close()
+    prof.export_chrome_trace(os.environ.get("DIAG_TRACE_OUT", "/tmp/diag_trace.json"))
+    evs = []
+    for e in prof.events():
+        evs.append({"name": e.name[:60], "dev": str(e.device_type), "start_us": e.time_range.start,
+                    "dur_us": e.time_range.end - e.time_range.start})
+    evs.sort(key=lambda x: x["start_us"])
+    t0 = evs[0]["start_us"] if evs else 0
+    for x in evs:
+        x["start_us"] -= t0
+    return evs
+
+
+class _Null:
+    def __enter__(self):
+        return None
+
+    def __exit__(self, *a):
+        return False
+
+
+if __name__ == "__main__" and os.environ.get("DIAG_TRACE"):
+    torch.cuda.set_device(0)
+    for x in trace(verify=os.environ.get("DIAG_TRACE") == "1"):
+        print(json.dumps(x))
