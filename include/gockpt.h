@@ -332,7 +332,11 @@ gck_status gck_plan_parts(uint64_t n, uint32_t K, uint32_t A, uint64_t *lo_hi);
 /* a5, host: replay a staged session in place. master/m/v: host arrays of n
  * floats holding part j at S(t0+j-1); glog[i-1]: host bf16 array of >= hi_i
  * elements (i = 1..K-1); recs[i-1]: StepRecord of update t0+i. Runs on
- * `threads` threads (0 = all cores). Host-only; usable without a GPU. */
+ * `threads` threads (0 = all cores). Host-only; usable without a GPU. Side effect on the CPU
+ * caches only: the lines of the last ~2 x (L2s + L3) bytes it touched are written back and evicted
+ * (clflushopt), so a following DMA into the same pinned memory does not snoop other cores' caches
+ * (GCK_EVICT_BYTES=<bytes> overrides the amount, 0 = off; gck_checksum and the persist writers
+ * do the same). */
 gck_status gck_replay_host(const gck_step_record *recs, uint32_t K, const uint64_t *lo_hi, uint64_t n,
                            float *master, float *m, float *v, const uint16_t *const *glog, int32_t threads);
 
