@@ -280,7 +280,7 @@ gck_status write_checkpoint_impl(const char *path, const gck_file_header *hdr_in
     bool ok = pwrite_all(fd, tbl.data(), tbl.size(), L.table_off);
     if (log && ok) {  // the replay log header + gradient CRC table, before the file header
         std::vector<char> gt(G.table_bytes, 0);
-        std::memcpy(gt.data(), gtable.data(), gtable.size() * 4);
+        if (!gtable.empty()) std::memcpy(gt.data(), gtable.data(), gtable.size() * 4);  // K = 1: no slices
         gck_log_header lh;
         std::memset(&lh, 0, sizeof(lh));
         std::memcpy(lh.magic, GCK_LOG_MAGIC, 8);
