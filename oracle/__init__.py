@@ -27,16 +27,17 @@ Pins (tests/test_oracle_*.py, all ``-m "not gpu"``): SPEC's scalar examples,
 the hand-worked K=2 example (tests/golden/k2_example.txt), a float64 closed
 form for constant gradients, torch.optim.AdamW in float64, brute force O2==O1
 over every contiguous partition of tiny vectors, the paper's K=3 version trace,
-SPEC's make_parts examples and closed-form byte counts. No function here is
+SPEC's make_parts examples and closed-form byte counts; the balanced plan against
+brute-force minima over every partition and the continuous optimum. No function here is
 "parity unpinned".
 """
 
 from .adamw import StepRecord, make_step_record, adamw_update, rne_bf16, bf16_to_f32, trajectory
-from .partition import make_parts, grad_prefix, session_bytes, slot_bytes
+from .partition import make_parts, make_parts_balanced, max_slot_bytes, grad_prefix, session_bytes, slot_bytes
 from .replay import capture_session, replay, replay_streaming, assemble, oracle_session
 
 __all__ = [
     "StepRecord", "make_step_record", "adamw_update", "rne_bf16", "bf16_to_f32", "trajectory",
-    "make_parts", "grad_prefix", "session_bytes", "slot_bytes",
+    "make_parts", "make_parts_balanced", "max_slot_bytes", "grad_prefix", "session_bytes", "slot_bytes",
     "capture_session", "replay", "replay_streaming", "assemble", "oracle_session",
 ]
