@@ -99,6 +99,9 @@ def parse():
     ap.add_argument("--verify-drain", type=int, default=1,
                     help="1 (library default): checksum every drained slice on the device and the host "
                          "(a3 verification); 0: off")
+    ap.add_argument("--plan", choices=["equal", "balanced"], default="equal",
+                    help="partition plan (a1): equal parts (S:131, the paper's default) or the transfer-balanced "
+                         "plan (DESIGN.md R17: the parts that minimise the largest per-step D2H)")
     ap.add_argument("--force-collectives", action="store_true",
                     help="run the NCCL reduce-scatter / all-gather path even at N = 1 (a process group of one; "
                          "needs the torchrun environment or MASTER_ADDR/MASTER_PORT)")
@@ -152,7 +155,7 @@ def ncu_traffic():
 _ORACLE_INPUTS = {}
 
 
-def oracle_interval_seconds(n_sample: int, K: int, interval: int, seed: int = 42) -> tuple[float, int]:
+def oracle_interval_seconds(n_sample: int, K: int, interval: int, seed: int = 42, plan: str = "equal") -> tuple[float, int]:
     """Time the oracle on the CPU work of one checkpoint interval over n_sample elements:
     `interval` AdamW updates (O1 trajectory) with a K-part session (capture + O2 replay).
     The seeded inputs are generated once per sample size (outside the timed region)."""
@@ -169,7 +172,8 @@ def oracle_interval_seconds(n_sample: int, K: int, interval: int, seed: int = 42
                                [oracle.make_step_record(t=T_WARM + s, lr=LR, **HP) for s in range(1, interval + 1)])
     (p, m, v), grads, recs = _ORACLE_INPUTS[key]
     t_start = time.perf_counter()
-    parts = oracle.make_parts(n_sample, K, min(1024, max(1, n_sample // K)))
+    mk = oracle.make_parts_balanced if plan == "balanced" else oracle.make_parts
+    parts = mk(n_sample, K, min(1024, max(1, n_sample // K)))
     cap, glog, live = oracle.capture_session(p, m, v, grads[:K], recs[:K], parts)   # session steps 1..K
     ck = oracle.replay(cap, glog, recs[:K], parts)
     p, m, v = live
@@ -201,8 +205,8 @@ def oracle_baseline(args, K, steps=1, warmup=0):
     n_s = min(args.cpu_sample, args.n)
     with OneCore() as oc:
         for _ in range(warmup):
-            oracle_interval_seconds(n_s, K, args.interval)
-        times = [oracle_interval_seconds(n_s, K, args.interval)[0] for _ in range(steps)]
+            oracle_interval_seconds(n_s, K, args.interval, plan=args.plan)
+        times = [oracle_interval_seconds(n_s, K, args.interval, plan=args.plan)[0] for _ in range(steps)]
     per_sample = statistics.mean(times)
     factor = args.n / n_s
     per_interval = per_sample * factor
@@ -249,7 +253,7 @@ def config_dict(args, world):
             "fb_standin": fb,
             "fb_tflop_per_step": 0.0 if args.model == "flat-1m" else standin_flops(args.model, args.tokens) / 1e12,
             "copy_mode": args.copy_mode, "ring_slots": args.ring_slots, "staging": args.staging,
-            "verify_drain": bool(args.verify_drain),
+            "verify_drain": bool(args.verify_drain), "plan": args.plan,
             "scheme": args.scheme, "replay_mode": args.replay_mode,
             "dist_backend": args.dist_backend if world > 1 else None,
             "rs_bucket_mb": args.rs_bucket_mb if (world > 1 or getattr(args, "force_collectives", False))
@@ -374,7 +378,7 @@ def main():
                    part_align=1024,
                    ring_slots=args.ring_slots, copy_mode=args.copy_mode, replay_threads=args.replay_threads,
                    timing=True, eager_replay=True, staging=args.staging, replay_mode=args.replay_mode,
-                   stream_buffers=args.stream_buffers, verify_drain=bool(args.verify_drain))
+                   stream_buffers=args.stream_buffers, verify_drain=bool(args.verify_drain), plan=args.plan)
     baseline = args.scheme != "gockpt"
     if baseline:
         snap_host = [torch.empty(n, dtype=torch.float32, pin_memory=True) for _ in range(3)]
@@ -531,7 +535,7 @@ def main():
     torch.cuda.synchronize()
     K = state["K"]
     state["auto"] = False
-    parts = G.plan_parts(n, K, 1024)
+    parts = G.plan_parts(n, K, 1024, plan=args.plan)
     session_bytes = sum(12 * (hi - lo) + (2 * hi if i < K - 1 else 0) for i, (lo, hi) in enumerate(parts))
 
     # ---- checkpoint-free reference, first half (the second half runs after the timed region, so
@@ -650,7 +654,7 @@ def main():
                     "slot": (None if e["slot"] == 0xFFFFFFFF else e["slot"]) if e else None}) + "\n")
     # NEXT-4: the analytic model's K for this step time and link (smallest K whose largest per-step
     # transfer fits in one step), next to the K this run used
-    k_rec, vmax_rec = G.recommend_k(n, link_peak, free_med / 1e3, 1.0, 64)
+    k_rec, vmax_rec = G.recommend_k(n, link_peak, free_med / 1e3, 1.0, 64, plan=args.plan)
     line = {
         "metric": METRIC,
         "value": value,

@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define GCK_ABI_VERSION 1u
+#define GCK_ABI_VERSION 2u /* 2: gck_config.plan, plan arguments of ring sizing and K selection */
 #define GCK_K_LIMIT 64u /* largest K a session may use */
 
 typedef enum {
@@ -76,6 +76,12 @@ typedef struct {
 enum { GCK_COPY_ENGINE = 0, GCK_COPY_ZEROCOPY = 1 };
 enum { GCK_REPLAY_HOST = 0, GCK_REPLAY_GPU = 1, GCK_REPLAY_DEFERRED = 2, GCK_REPLAY_STREAM = 3 };
 enum { GCK_STAGE_RING = 0, GCK_STAGE_DIRECT = 1, GCK_STAGE_BLOCKING = 2 };
+/* Partition plans (a1). EQUAL: K parts of equal size over A-element units, remainder to the earliest
+ * parts (R11). BALANCED (ours, R17; the paper leaves the part sizes
+ * open): the contiguous unit-aligned parts that minimise the largest per-step transfer
+ * V_max = max_i 12|P_i| + 2 hi_i [i<K] — early parts larger, later ones smaller — kept only when it
+ * beats EQUAL; V_max 2.42n vs 3.25n at K = 8. The checkpoint S(T) is the same under either plan. */
+enum { GCK_PLAN_EQUAL = 0, GCK_PLAN_BALANCED = 1 };
 
 typedef struct {
     uint32_t abi_version;   /* must be GCK_ABI_VERSION */
@@ -132,6 +138,8 @@ typedef struct {
                                recomputes the checksum of the landed bytes before the replay uses them
                                (A = sum w_i, B = sum (i+1) w_i mod 2^64 over 32-bit words); a mismatch
                                voids the session with GCK_E_CORRUPT. 0: no verification */
+    int32_t plan;           /* GCK_PLAN_EQUAL (0) or GCK_PLAN_BALANCED: the partition plan of every session;
+                               also sizes the ring and the gradient log */
 } gck_config;
 
 /* Caller-owned device tensors (PyTorch owns them; they must outlive the context). */
@@ -225,9 +233,10 @@ typedef struct {
 
 /* ---- context lifecycle -------------------------------------------------- */
 
-/* HBM bytes the ring needs for (n, K in [k_min, k_max], A, R slots): R x the largest
+/* HBM bytes the ring needs for (n, K in [k_min, k_max], A, R slots, plan): R x the largest
  * 256-B-aligned [master_i | m_i | v_i | G[0:hi_i]] slot. Host-only. 0 on invalid input. */
-uint64_t gck_ring_bytes_required(uint64_t n, uint32_t k_min, uint32_t k_max, uint32_t part_align, uint32_t ring_slots);
+uint64_t gck_ring_bytes_required(uint64_t n, uint32_t k_min, uint32_t k_max, uint32_t part_align, uint32_t ring_slots,
+                                 int32_t plan);
 
 /* Validate, create the D2H stream + events, allocate the HBM staging ring
  * (R slots sized for K in [k_min, k_max]) and the pinned host arena
@@ -325,9 +334,12 @@ const char *gck_last_error(const gck_ctx *ctx);
 gck_status gck_make_step_record(const gck_hparams *hp, uint64_t adam_t, double lr, double grad_scale,
                                 int32_t skip, gck_step_record *out);
 
-/* a1: the K part ranges of [0, n) with alignment A; lo_hi[2i], lo_hi[2i+1] =
+/* a1: the K part ranges of [0, n) with alignment A under the EQUAL plan; lo_hi[2i], lo_hi[2i+1] =
  * lo_{i+1}, hi_{i+1}. Host-only. Errors: INVALID. */
 gck_status gck_plan_parts(uint64_t n, uint32_t K, uint32_t A, uint64_t *lo_hi);
+/* a1 under either plan (GCK_PLAN_EQUAL / GCK_PLAN_BALANCED, R17); same layout. Host-only.
+ * Errors: INVALID (n = 0, A = 0, K = 0, K > ceil(n/A), K > GCK_K_LIMIT, bad plan). */
+gck_status gck_plan_parts_mode(uint64_t n, uint32_t K, uint32_t A, int32_t plan, uint64_t *lo_hi);
 
 /* a5, host: replay a staged session in place. master/m/v: host arrays of n
  * floats holding part j at S(t0+j-1); glog[i-1]: host bf16 array of >= hi_i
@@ -492,11 +504,11 @@ double gck_model_optimal_waste(double t_ckpt, double p_fail, double t_load);
  * share = 1/7 in the paper's formula, 1/6 for a 12-B state + 2-B gradient, R4). */
 double gck_model_stall_async_o(uint32_t N, double t_step);
 double gck_model_stall_gockpt(uint32_t N, double t_step, double grad_share);
-/* Smallest K in [1, k_max] whose largest per-step D2H V_max(K) (a1 plan with alignment A)
+/* Smallest K in [1, k_max] whose largest per-step D2H V_max(K) (a1 plan `plan` with alignment A)
  * takes at most budget x t_step at link_gbs GB/s (SURVEY §8(d) K_min). *k_out = 0 and
  * GCK_E_INVALID if none does. v_max_bytes (nullable) receives V_max of the chosen K. */
-gck_status gck_recommend_k(uint64_t n, uint32_t part_align, double link_gbs, double t_step_s, double budget,
-                           uint32_t k_max, uint32_t *k_out, double *v_max_bytes);
+gck_status gck_recommend_k(uint64_t n, uint32_t part_align, int32_t plan, double link_gbs, double t_step_s,
+                           double budget, uint32_t k_max, uint32_t *k_out, double *v_max_bytes);
 
 /* ---- harness-only (NOT the method): seeded synthetic inputs ------------- */
 

@@ -17,7 +17,8 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 # scripts/build_asan.sh); the default is the in-tree sm_100a build.
 LIB_PATH = os.environ.get("GCK_LIB_PATH") or os.path.join(_HERE, "libgockpt.so")
 
-ABI_VERSION = 1
+ABI_VERSION = 2
+PLAN_EQUAL, PLAN_BALANCED = 0, 1
 K_LIMIT = 64
 
 (OK, E_INVALID, E_PROTOCOL, E_STALE, E_NOMEM, E_CUDA, E_INCOMPLETE, E_ABORTED, E_BUSY, E_NODEVICE, E_IO,
@@ -39,7 +40,8 @@ class Config(C.Structure):
                 ("ring_slots", C.c_uint32), ("copy_mode", C.c_int32), ("chunk_bytes", C.c_uint64),
                 ("zc_ctas", C.c_uint32), ("replay_mode", C.c_int32), ("replay_threads", C.c_int32),
                 ("timing", C.c_int32), ("eager_replay", C.c_int32), ("staging", C.c_int32),
-                ("numa_node", C.c_int32), ("stream_buffers", C.c_uint32), ("verify_drain", C.c_int32)]
+                ("numa_node", C.c_int32), ("stream_buffers", C.c_uint32), ("verify_drain", C.c_int32),
+                ("plan", C.c_int32)]
 
 
 class Tensors(C.Structure):
@@ -141,6 +143,7 @@ SIGNATURES = {
     "gck_make_step_record": (C.c_int, [C.POINTER(Hparams), C.c_uint64, C.c_double, C.c_double, C.c_int32,
                                        C.POINTER(StepRecord)]),
     "gck_plan_parts": (C.c_int, [C.c_uint64, C.c_uint32, C.c_uint32, U64P]),
+    "gck_plan_parts_mode": (C.c_int, [C.c_uint64, C.c_uint32, C.c_uint32, C.c_int32, U64P]),
     "gck_replay_host": (C.c_int, [C.POINTER(StepRecord), C.c_uint32, U64P, C.c_uint64, P, P, P,
                                   C.POINTER(P), C.c_int32]),
     "gck_replay_device": (C.c_int, [C.POINTER(StepRecord), C.c_uint32, U64P, C.c_uint64, P, P, P,
@@ -169,9 +172,10 @@ SIGNATURES = {
     "gck_model_optimal_waste": (C.c_double, [C.c_double] * 3),
     "gck_model_stall_async_o": (C.c_double, [C.c_uint32, C.c_double]),
     "gck_model_stall_gockpt": (C.c_double, [C.c_uint32, C.c_double, C.c_double]),
-    "gck_recommend_k": (C.c_int, [C.c_uint64, C.c_uint32, C.c_double, C.c_double, C.c_double, C.c_uint32,
+    "gck_recommend_k": (C.c_int, [C.c_uint64, C.c_uint32, C.c_int32, C.c_double, C.c_double, C.c_double, C.c_uint32,
                                   C.POINTER(C.c_uint32), C.POINTER(C.c_double)]),
-    "gck_ring_bytes_required": (C.c_uint64, [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32]),
+    "gck_ring_bytes_required": (C.c_uint64, [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                             C.c_int32]),
     "gck_device_count": (C.c_int32, []),
 }
 

@@ -93,6 +93,60 @@ gck_status plan_parts(uint64_t n, uint32_t K, uint32_t A, uint64_t *lo, uint64_t
     return GCK_OK;
 }
 
+// V_max of a plan: the largest per-step D2H, 12 |P_i| + 2 hi_i (i < K), 12 |P_K| (a1).
+uint64_t plan_vmax(uint32_t K, const uint64_t *lo, const uint64_t *hi) {
+    uint64_t v = 0;
+    for (uint32_t i = 0; i < K; ++i) v = std::max(v, 12 * (hi[i] - lo[i]) + (i + 1 < K ? 2 * hi[i] : 0));
+    return v;
+}
+
+// Greedy fill at byte budget V (R17): parts 1..K-1 each take the most whole units u
+// with 12 A u + 2 A (H + u) <= V, at least one, leaving one unit for every later part; the last
+// part takes the rest.
+void fill_balanced(uint64_t n, uint32_t K, uint64_t A, uint64_t U, uint64_t V, uint64_t *lo, uint64_t *hi) {
+    uint64_t H = 0;
+    for (uint32_t i = 1; i < K; ++i) {
+        const uint64_t cap = V >= 2 * A * H ? (V - 2 * A * H) / (14 * A) : 0;
+        const uint64_t u = std::min<uint64_t>(std::max<uint64_t>(cap, 1), U - H - (K - i));
+        lo[i - 1] = H * A;
+        H += u;
+        hi[i - 1] = H * A;
+    }
+    lo[K - 1] = H * A;
+    hi[K - 1] = n;
+}
+
+// The transfer-balanced plan (R17): the greedy fill at the smallest integer budget V in [0, 14 n]
+// whose fill keeps every V_i <= V (binary search), unless it is not strictly better than the equal
+// plan. Bit-identical to oracle.partition.make_parts_balanced.
+gck_status plan_parts_balanced(uint64_t n, uint32_t K, uint32_t A, uint64_t *lo, uint64_t *hi) {
+    gck_status st = plan_parts(n, K, A, lo, hi);  // the equal plan; also validates n, K, A
+    if (st != GCK_OK || K == 1) return st;
+    const uint64_t U = (n + A - 1) / A;
+    uint64_t blo = 0, bhi = 14 * n;
+    uint64_t tl[GCK_K_LIMIT], th[GCK_K_LIMIT];
+    while (blo < bhi) {
+        const uint64_t mid = blo + (bhi - blo) / 2;
+        fill_balanced(n, K, A, U, mid, tl, th);
+        if (plan_vmax(K, tl, th) <= mid)
+            bhi = mid;
+        else
+            blo = mid + 1;
+    }
+    fill_balanced(n, K, A, U, blo, tl, th);
+    if (plan_vmax(K, tl, th) < plan_vmax(K, lo, hi)) {
+        std::memcpy(lo, tl, K * sizeof(uint64_t));
+        std::memcpy(hi, th, K * sizeof(uint64_t));
+    }
+    return GCK_OK;
+}
+
+gck_status plan_parts_mode(uint64_t n, uint32_t K, uint32_t A, int32_t plan, uint64_t *lo, uint64_t *hi) {
+    if (plan == GCK_PLAN_BALANCED) return plan_parts_balanced(n, K, A, lo, hi);
+    if (plan != GCK_PLAN_EQUAL) return GCK_E_INVALID;
+    return plan_parts(n, K, A, lo, hi);
+}
+
 // Slot layout of session step i: [master | m | v | grad], each section 256-B aligned.
 struct SlotLayout {
     uint64_t off_m, off_v, off_g, bytes;
@@ -107,13 +161,14 @@ SlotLayout slot_layout(uint64_t part_elems, uint64_t grad_elems) {
     return s;
 }
 
-void ring_sizes(uint64_t n, uint32_t k_min, uint32_t k_max, uint32_t A, uint64_t *slot_max, uint64_t *glog_max) {
+void ring_sizes(uint64_t n, uint32_t k_min, uint32_t k_max, uint32_t A, int32_t plan, uint64_t *slot_max,
+                uint64_t *glog_max) {
     *slot_max = *glog_max = 0;
     const uint64_t U = (n + A - 1) / A;
     const uint32_t kmax_eff = (uint32_t)std::min<uint64_t>(k_max, U);
     for (uint32_t K = k_min; K <= kmax_eff; ++K) {
         uint64_t lo[GCK_K_LIMIT], hi[GCK_K_LIMIT];
-        plan_parts(n, K, A, lo, hi);
+        plan_parts_mode(n, K, A, plan, lo, hi);
         uint64_t gsum = 0;
         for (uint32_t i = 0; i < K; ++i) {
             const uint64_t ghi = (i + 1 < K) ? hi[i] : 0;
@@ -689,20 +744,26 @@ gck_status gck_make_step_record(const gck_hparams *hp, uint64_t adam_t, double l
 }
 
 uint64_t gck_ring_bytes_required(uint64_t n, uint32_t k_min, uint32_t k_max, uint32_t part_align,
-                                 uint32_t ring_slots) {
+                                 uint32_t ring_slots, int32_t plan) {
     const uint32_t A = part_align ? part_align : 1024;
     const uint32_t R = ring_slots ? ring_slots : 2;
     if (n == 0 || k_min == 0 || k_max < k_min || k_max > GCK_K_LIMIT || R > 2 || (A % 8)) return 0;
+    if (plan != GCK_PLAN_EQUAL && plan != GCK_PLAN_BALANCED) return 0;
     uint64_t slot = 0, glog = 0;
-    ring_sizes(n, k_min, k_max, A, &slot, &glog);
+    ring_sizes(n, k_min, k_max, A, plan, &slot, &glog);
     return slot * R;
 }
 
 gck_status gck_plan_parts(uint64_t n, uint32_t K, uint32_t A, uint64_t *lo_hi) {
+    return gck_plan_parts_mode(n, K, A, GCK_PLAN_EQUAL, lo_hi);
+}
+
+gck_status gck_plan_parts_mode(uint64_t n, uint32_t K, uint32_t A, int32_t plan, uint64_t *lo_hi) {
     if (!lo_hi) return set_tls(GCK_E_INVALID, "null lo_hi");
+    if (plan != GCK_PLAN_EQUAL && plan != GCK_PLAN_BALANCED) return set_tls(GCK_E_INVALID, "bad plan");
     uint64_t lo[GCK_K_LIMIT], hi[GCK_K_LIMIT];
     if (K > GCK_K_LIMIT) return set_tls(GCK_E_INVALID, "K exceeds GCK_K_LIMIT");
-    gck_status st = plan_parts(n, K, A, lo, hi);
+    gck_status st = plan_parts_mode(n, K, A, plan, lo, hi);
     if (st != GCK_OK) return set_tls(st, "need n >= 1, A >= 1, 1 <= K <= ceil(n/A)");
     for (uint32_t i = 0; i < K; ++i) {
         lo_hi[2 * i] = lo[i];
@@ -816,6 +877,7 @@ gck_status gck_create(const gck_config *cfg_in, const gck_hparams *hp, const gck
     if (cfg.part_align % 8) return set_tls(GCK_E_INVALID, "part_align must be a multiple of 8");
     if (cfg.k_max < cfg.k_min || cfg.k_max > GCK_K_LIMIT) return set_tls(GCK_E_INVALID, "need 1 <= k_min <= k_max <= 64");
     if (cfg.ring_slots > 2) return set_tls(GCK_E_INVALID, "ring_slots must be 1 or 2");
+    if (cfg.plan != GCK_PLAN_EQUAL && cfg.plan != GCK_PLAN_BALANCED) return set_tls(GCK_E_INVALID, "bad plan");
     if (cfg.staging != GCK_STAGE_RING && cfg.staging != GCK_STAGE_DIRECT && cfg.staging != GCK_STAGE_BLOCKING)
         return set_tls(GCK_E_INVALID, "bad staging");
     if (cfg.copy_mode != GCK_COPY_ENGINE && cfg.copy_mode != GCK_COPY_ZEROCOPY)
@@ -848,7 +910,7 @@ gck_status gck_create(const gck_config *cfg_in, const gck_hparams *hp, const gck
 
     // sizes: worst case over K in [k_min, min(k_max, U)]
     uint64_t slot_max = 0, glog_max = 0;
-    ring_sizes(cfg.n, cfg.k_min, cfg.k_max, cfg.part_align, &slot_max, &glog_max);
+    ring_sizes(cfg.n, cfg.k_min, cfg.k_max, cfg.part_align, cfg.plan, &slot_max, &glog_max);
     c->direct = (cfg.staging == GCK_STAGE_DIRECT || cfg.staging == GCK_STAGE_BLOCKING);
     c->blocking_grad = (cfg.staging == GCK_STAGE_BLOCKING);
     c->slot_bytes = c->direct ? 0 : slot_max;
@@ -867,7 +929,7 @@ gck_status gck_create(const gck_config *cfg_in, const gck_hparams *hp, const gck
         uint64_t largest = 0;  // the largest gradient slice G[0:hi_{K-1}] over K in [k_min, k_max]
         for (uint32_t K = std::max<uint32_t>(2, cfg.k_min); K <= kmax_eff; ++K) {
             uint64_t lo[GCK_K_LIMIT], hi[GCK_K_LIMIT];
-            plan_parts(cfg.n, K, cfg.part_align, lo, hi);
+            plan_parts_mode(cfg.n, K, cfg.part_align, cfg.plan, lo, hi);
             largest = std::max(largest, hi[K - 2]);
         }
         c->slice_elems = align_up(largest, 128);
@@ -1061,7 +1123,9 @@ static uint32_t auto_k(gck_ctx *c) {
     c->stats.auto_step_ms = t_step * 1e3;
     c->stats.auto_link_gbs = gbs;
     uint32_t k = 0;
-    if (gck_recommend_k(c->cfg.n, c->cfg.part_align, gbs, t_step, 1.0, c->cfg.k_max, &k, nullptr) != GCK_OK || k == 0)
+    if (gck_recommend_k(c->cfg.n, c->cfg.part_align, c->cfg.plan, gbs, t_step, 1.0, c->cfg.k_max, &k, nullptr) !=
+            GCK_OK ||
+        k == 0)
         return c->cfg.k_max;
     return std::max(k, c->cfg.k_min);
 }
@@ -1082,7 +1146,7 @@ gck_status gck_begin_checkpoint(gck_ctx *c, uint64_t t0, uint32_t K) {
         cudaStreamSynchronize(c->d2h);
         cudaGetLastError();
     }
-    if (plan_parts(c->cfg.n, K, c->cfg.part_align, c->lo, c->hi) != GCK_OK)
+    if (plan_parts_mode(c->cfg.n, K, c->cfg.part_align, c->cfg.plan, c->lo, c->hi) != GCK_OK)
         return c->fail(GCK_E_INVALID, "K exceeds ceil(n/A)");
     uint64_t off = 0;
     for (uint32_t i = 0; i < K; ++i) {

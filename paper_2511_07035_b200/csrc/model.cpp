@@ -7,7 +7,8 @@
 //                with r the gradient share of a part's bytes (the paper's 1/7; 1/6 for this build's
 //                12-B state + 2-B gradient, R4)
 //  K selection (ours): the smallest K whose largest per-step D2H
-//                V_max(K) = 12|P_{K-1}| + 2 hi_{K-1} fits in `budget` x T_step at bandwidth BW.
+//                V_max(K) = max_i 12|P_i| + 2 hi_i [i<K] under the session's plan (equal: step K-1;
+//                balanced, R17: about equal on every step) fits in `budget` x T_step at BW.
 #include <cmath>
 
 #include "internal.h"
@@ -32,14 +33,14 @@ double gck_model_stall_gockpt(uint32_t N, double t_step, double grad_share) {
     return grad_share * N * (N - 1.0) / 2.0 * t_step;
 }
 
-gck_status gck_recommend_k(uint64_t n, uint32_t part_align, double link_gbs, double t_step_s, double budget,
-                           uint32_t k_max, uint32_t *k_out, double *v_max_bytes) {
+gck_status gck_recommend_k(uint64_t n, uint32_t part_align, int32_t plan, double link_gbs, double t_step_s,
+                           double budget, uint32_t k_max, uint32_t *k_out, double *v_max_bytes) {
     if (!k_out || n == 0 || link_gbs <= 0 || t_step_s <= 0 || budget <= 0 || k_max == 0 || k_max > GCK_K_LIMIT)
         return GCK_E_INVALID;
     const uint32_t A = part_align ? part_align : 1024;
     uint64_t lo_hi[2 * GCK_K_LIMIT];
     for (uint32_t K = 1; K <= k_max; ++K) {
-        if (gck_plan_parts(n, K, A, lo_hi) != GCK_OK) break;
+        if (gck_plan_parts_mode(n, K, A, plan, lo_hi) != GCK_OK) break;
         uint64_t vmax = 0;
         for (uint32_t i = 0; i < K; ++i) {
             const uint64_t part = lo_hi[2 * i + 1] - lo_hi[2 * i];

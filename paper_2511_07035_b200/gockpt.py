@@ -55,10 +55,13 @@ def make_step_record(beta1, beta2, eps, weight_decay, adam_t, lr, grad_scale=1.0
     return rec
 
 
-def plan_parts(n: int, K: int, A: int = 1024):
-    """a1 (gck_plan_parts) -> [(lo, hi), ...]."""
+PLANS = {"equal": L.PLAN_EQUAL, "balanced": L.PLAN_BALANCED}
+
+
+def plan_parts(n: int, K: int, A: int = 1024, plan: str = "equal"):
+    """a1 (gck_plan_parts_mode) -> [(lo, hi), ...]; plan "equal" or "balanced" (R17)."""
     buf = (C.c_uint64 * (2 * K))()
-    check(lib().gck_plan_parts(n, K, A, buf))
+    check(lib().gck_plan_parts_mode(n, K, A, PLANS[plan], buf))
     return [(buf[2 * i], buf[2 * i + 1]) for i in range(K)]
 
 
@@ -195,10 +198,11 @@ def load_checkpoint_range(path: str, offset: int, count: int, out=None, threads:
     return out[0], out[1], out[2], _hdr_dict(h)
 
 
-def recommend_k(n: int, link_gbs: float, t_step_s: float, budget: float = 1.0, k_max: int = 16, A: int = 1024):
+def recommend_k(n: int, link_gbs: float, t_step_s: float, budget: float = 1.0, k_max: int = 16, A: int = 1024,
+                plan: str = "equal"):
     """NEXT-4 (gck_recommend_k) -> (K, V_max bytes); K = 0 if none fits."""
     k, vmax = C.c_uint32(0), C.c_double(0)
-    st = lib().gck_recommend_k(n, A, link_gbs, t_step_s, budget, k_max, C.byref(k), C.byref(vmax))
+    st = lib().gck_recommend_k(n, A, PLANS[plan], link_gbs, t_step_s, budget, k_max, C.byref(k), C.byref(vmax))
     if st not in (L.OK, L.E_INVALID):
         check(st)
     return k.value, vmax.value
@@ -213,8 +217,9 @@ def h_generate(kind, out, seed, step=0, offset=0, mode=0, zero_per_256=4, stream
                                _stream_ptr(stream)))
 
 
-def ring_bytes_required(n: int, k_min: int, k_max: int, part_align: int = 1024, ring_slots: int = 2) -> int:
-    return int(lib().gck_ring_bytes_required(n, k_min, k_max, part_align, ring_slots))
+def ring_bytes_required(n: int, k_min: int, k_max: int, part_align: int = 1024, ring_slots: int = 2,
+                        plan: str = "equal") -> int:
+    return int(lib().gck_ring_bytes_required(n, k_min, k_max, part_align, ring_slots, PLANS[plan]))
 
 
 def device_count() -> int:
@@ -238,7 +243,8 @@ class GoCkpt:
     def __init__(self, master, exp_avg, exp_avg_sq, param_bf16=None, *, beta1=0.9, beta2=0.999, eps=1e-8,
                  weight_decay=0.01, k_min=1, k_max=8, part_align=1024, ring_slots=2, copy_mode="ce",
                  chunk_bytes=0, zc_ctas=0, replay_threads=0, timing=True, eager_replay=True, staging="ring",
-                 numa_node=-1, replay_mode="host", ring=None, stream_buffers=0, verify_drain=True):
+                 numa_node=-1, replay_mode="host", ring=None, stream_buffers=0, verify_drain=True,
+                 plan="equal"):
         n = master.numel()
         if exp_avg.numel() != n or exp_avg_sq.numel() != n or (param_bf16 is not None and param_bf16.numel() != n):
             raise ValueError("state tensors must have the same number of elements")
@@ -251,7 +257,7 @@ class GoCkpt:
                        replay_threads, int(timing),
                        int(eager_replay),
                        {"ring": L.STAGE_RING, "direct": L.STAGE_DIRECT, "blocking": L.STAGE_BLOCKING}[staging],
-                       numa_node, stream_buffers, int(verify_drain))
+                       numa_node, stream_buffers, int(verify_drain), PLANS[plan])
         hp = L.Hparams(beta1, beta2, eps, weight_decay)
         self.hparams = dict(beta1=beta1, beta2=beta2, eps=eps, weight_decay=weight_decay)
         # ring: an optional caller-owned uint8 CUDA tensor of >= ring_bytes_required(...) bytes

@@ -92,3 +92,19 @@ def test_recommend_k(L):
     # SURVEY §8(d) worked examples at 55 GB/s: 13B/8 at 0.12 s -> 5; GPT-2 at 10 ms -> 5
     assert G.recommend_k(1_626_983_040, 55.0, 0.12)[0] == 5
     assert G.recommend_k(n, 55.0, 0.010)[0] == 5
+
+
+def test_recommend_k_balanced_plan(L):
+    # the same rule under the transfer-balanced plan (R17): its V_max is never larger, so
+    # the recommended K is never larger either; at 13B/4 on a 167 ms step: K = 12 -> a smaller K
+    import paper_2511_07035_b200 as G
+    from oracle import make_parts_balanced, max_slot_bytes
+    for n, bw, ts in [(124_439_808, 57.0, 0.0167), (3_253_966_336, 57.0, 0.167), (1_626_983_040, 55.0, 0.12),
+                      (6_507_932_160, 57.0, 0.184)]:
+        ke, _ = G.recommend_k(n, bw, ts)
+        kb, vb = G.recommend_k(n, bw, ts, plan="balanced")
+        if kb:
+            assert vb == max_slot_bytes(make_parts_balanced(n, kb, 1024)) and vb / (bw * 1e9) <= ts
+            assert kb == 1 or max_slot_bytes(make_parts_balanced(n, kb - 1, 1024)) / (bw * 1e9) > ts
+        assert ke == 0 or (kb and kb <= ke)
+    assert G.recommend_k(3_253_966_336, 57.0, 0.167, plan="balanced")[0] < G.recommend_k(3_253_966_336, 57.0, 0.167)[0]

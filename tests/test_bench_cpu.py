@@ -68,7 +68,7 @@ def test_reference_and_gpu_arm_share_the_config():
     bench = importlib.import_module("bench")
     a = type("A", (), dict(model="gpt2-small", shard_of=0, n=0, tokens=0, K=8, interval=50, copy_mode="ce",
                            ring_slots=2, staging="ring", scheme="gockpt", replay_mode="host",
-                           dist_backend="nccl", rs_bucket_mb=512, spin_ms=1.0, verify_drain=1))()
+                           dist_backend="nccl", rs_bucket_mb=512, spin_ms=1.0, verify_drain=1, plan="equal"))()
     bench.resolve(a)
     c1 = bench.config_dict(a, 1)
     assert dict(c1, K=8) == c1 and c1["fb_tflop_per_step"] > 10 and c1["n_per_rank"] == 124_439_808

@@ -82,13 +82,14 @@ def test_fused_step_trajectory_vs_oracle(G, n):
     (300_007, 64, 8, 2, "ce"),              # K = GCK_K_LIMIT (maximum), TMA kernel, parts not tile-aligned
 ])
 @pytest.mark.parametrize("seed", [42, 7])
-def test_session_staged_replays_and_snapshot(G, n, K, A, R, copy, seed):
+@pytest.mark.parametrize("plan", ["equal", "balanced"])
+def test_session_staged_replays_and_snapshot(G, n, K, A, R, copy, seed, plan):
     t0 = 10
     state, grads, recs, sargs = session_inputs(seed, n, K, t0)
     ctx, (p, m, v, out) = _make_ctx(G, state, K, part_align=A, ring_slots=R, copy_mode=copy, eager_replay=False,
-                                    chunk_bytes=(1 << 20) if copy == "ce" and R == 1 else 0)
-    parts = oracle.make_parts(n, K, A)
-    assert G.plan_parts(n, K, A) == parts
+                                    chunk_bytes=(1 << 20) if copy == "ce" and R == 1 else 0, plan=plan)
+    parts = (oracle.make_parts_balanced if plan == "balanced" else oracle.make_parts)(n, K, A)
+    assert G.plan_parts(n, K, A, plan=plan) == parts
     g_dev = [up_u16(g) for g in grads]
     ctx.begin_checkpoint(t0, K)
     snap = None
@@ -346,14 +347,15 @@ def test_persist_restore_resume_equals_uninterrupted(G, tmp_path, replay_mode, k
 @pytest.mark.parametrize("n,K,A,staging", [(1 << 20, 4, 1024, "ring"), (1_000_003, 8, 1024, "ring"),
                                            (300_007, 3, 8, "direct"), (5000, 1, 8, "ring"),
                                            ((1 << 18) + 4101, 16, 1024, "ring")])
-def test_deferred_replay_session_restore(G, tmp_path, n, K, A, staging):
+@pytest.mark.parametrize("plan", ["equal", "balanced"])
+def test_deferred_replay_session_restore(G, tmp_path, n, K, A, staging, plan):
     """replay_mode="deferred": finalize leaves the captured parts (== the oracle's capture, bit for
     bit), persist writes them with the gradient log, and the GPU restore (replay kernel in place on
     the device tensors) and the host loader both give the oracle's S(T) bit for bit."""
     t0, seed = 10, 13
     state, grads, recs, sargs = session_inputs(seed, n, K, t0, skips=(t0 + 2,) if K >= 3 else ())
-    ctx, (p, m, v, out) = _make_ctx(G, state, K, part_align=A, staging=staging, replay_mode="deferred")
-    parts = oracle.make_parts(n, K, A)
+    ctx, (p, m, v, out) = _make_ctx(G, state, K, part_align=A, staging=staging, replay_mode="deferred", plan=plan)
+    parts = (oracle.make_parts_balanced if plan == "balanced" else oracle.make_parts)(n, K, A)
     cap, glog, live = oracle.capture_session(*state, grads, recs, parts)
     want = oracle.trajectory(*state, grads[:K - 1], recs[:K - 1])[-1]
     ctx.begin_checkpoint(t0, K)
@@ -398,7 +400,8 @@ def test_deferred_replay_session_restore(G, tmp_path, n, K, A, staging):
                                                   (5000, 2, 8, 2, "ring", "ce"),
                                                   ((1 << 18) + 4101, 16, 1024, 4, "ring", "ce"),
                                                   (1 << 20, 1, 1024, 2, "ring", "ce")])
-def test_streaming_replay_session(G, n, K, A, B, staging, copy):
+@pytest.mark.parametrize("plan", ["equal", "balanced"])
+def test_streaming_replay_session(G, n, K, A, B, staging, copy, plan):
     """replay_mode="stream": slice i's update is applied to [0, hi_i) as soon as it drains, the
     gradient log is a ring of B buffers (the next drain into a buffer waits for its update).
     Result == the oracle's S(T) and == the GPU's own sync snapshot, bit for bit, with a skipped
@@ -406,7 +409,7 @@ def test_streaming_replay_session(G, n, K, A, B, staging, copy):
     t0, seed = 10, 19
     state, grads, recs, sargs = session_inputs(seed, n, K, t0, skips=(t0 + 2,) if K >= 3 else ())
     ctx, (p, m, v, out) = _make_ctx(G, state, K, part_align=A, staging=staging, copy_mode=copy,
-                                    replay_mode="stream", stream_buffers=B)
+                                    replay_mode="stream", stream_buffers=B, plan=plan)
     want = oracle.trajectory(*state, grads[:K - 1], recs[:K - 1])[-1]
     ctx.begin_checkpoint(t0, K)
     gbuf = None
@@ -457,7 +460,8 @@ def test_streaming_replay_session(G, n, K, A, B, staging, copy):
 @pytest.mark.parametrize("n,K,A,copy,staging", [(1 << 20, 4, 1024, "ce", "direct"), (1_000_003, 8, 1024, "ce", "direct"),
                                                 (300_007, 3, 8, "zerocopy", "direct"), (1 << 20, 1, 1024, "ce", "direct"),
                                                 (1_000_003, 4, 1024, "ce", "blocking")])
-def test_direct_staging_session(G, n, K, A, copy, staging):
+@pytest.mark.parametrize("plan", ["equal", "balanced"])
+def test_direct_staging_session(G, n, K, A, copy, staging, plan):
     """No HBM ring: part i is copied from the live arrays during step t0+i's F/B, the gradient
     prefix from ONE reused gradient buffer that the 'backward' overwrites right after
     gck_grad_fence. Staged bytes, host replay, GPU replay and snapshot as in ring mode."""
@@ -465,7 +469,7 @@ def test_direct_staging_session(G, n, K, A, copy, staging):
     state, grads, recs, sargs = session_inputs(seed, n, K, t0)
     p, m, v = (up_f32(x) for x in state)
     ctx = G.GoCkpt(p, m, v, None, **HP, k_min=1, k_max=max(K, 8), part_align=A, copy_mode=copy,
-                   eager_replay=False, staging=staging)
+                   eager_replay=False, staging=staging, plan=plan)
     gbuf = torch.empty(n, dtype=torch.int16, device="cuda")
     for s in range(1, 3):                                   # plain steps before the session
         gbuf.copy_(up_u16(gi.grad_bits(seed, 1000 + s, n)))
@@ -484,9 +488,10 @@ def test_direct_staging_session(G, n, K, A, copy, staging):
     ctx.grad_fence()
     gbuf.fill_(0)                                          # scribble the gradient buffer afterwards
     ctx.wait_drained()
-    parts = oracle.make_parts(n, K, A)
+    parts = (oracle.make_parts_balanced if plan == "balanced" else oracle.make_parts)(n, K, A)
     cap, glog, _ = oracle.capture_session(*state, grads, recs, parts)
     st = ctx.staged()
+    assert st["parts"] == parts
     assert_state_equal((st["master"], st["exp_avg"], st["exp_avg_sq"]), oracle.assemble(cap), "direct staged")
     for i in range(K - 1):
         assert np.array_equal(st["glog"][i], glog[i]), f"direct glog {i + 1}"

@@ -96,6 +96,7 @@ def test_create_validation_errors(G):
         L.Config(L.ABI_VERSION, 0, 1024, 1, 65, 8, 2, 0, 0, 0, 0, 0, 1, 1),      # k_max > 64
         L.Config(L.ABI_VERSION, 0, 1024, 1, 4, 8, 3, 0, 0, 0, 0, 0, 1, 1),       # R = 3
         L.Config(L.ABI_VERSION, 0, 64, 9, 9, 8, 2, 0, 0, 0, 0, 0, 1, 1),         # k_min > ceil(n/A)
+        L.Config(L.ABI_VERSION, 0, 1024, 1, 4, 8, 2, 0, 0, 0, 0, 0, 1, 1, plan=2),  # bad plan
     ]
     for cfg in bad:
         assert G.lib().gck_create(C.byref(cfg), C.byref(hp), C.byref(t), C.byref(ctx)) == L.E_INVALID
@@ -129,6 +130,28 @@ def test_step_record_errors(G):
                                    (124_439_808, 8, 1024), (3 * 1024 + 1, 4, 1024), (999, 64, 8)])
 def test_plan_parts_matches_oracle(G, n, K, A):
     assert G.plan_parts(n, K, A) == oracle.make_parts(n, K, A)
+
+
+@pytest.mark.parametrize("n,K,A", [(10, 3, 1), (10, 1, 1), (7, 7, 1), (2 ** 20, 4, 1024), (1_000_003, 4, 1024),
+                                   (124_439_808, 8, 1024), (3 * 1024 + 1, 4, 1024), (999, 64, 8),
+                                   (3_253_966_336, 16, 1024), (6_507_932_160, 16, 1024), (842_301_952, 64, 1024),
+                                   (4096, 2, 1), (13, 5, 2)])
+def test_plan_parts_balanced_matches_oracle(G, n, K, A):
+    # DESIGN.md R17: bit-identical plan (same integer rule); never a larger V_max than the equal plan
+    got = G.plan_parts(n, K, A, plan="balanced")
+    assert got == oracle.make_parts_balanced(n, K, A)
+    assert oracle.max_slot_bytes(got) <= oracle.max_slot_bytes(oracle.make_parts(n, K, A))
+    assert G.plan_parts(n, K, A, plan="equal") == oracle.make_parts(n, K, A)
+
+
+def test_plan_parts_balanced_sweep_matches_oracle(G):
+    rng = np.random.default_rng(5)
+    for _ in range(300):
+        A = int(rng.choice([1, 8, 1024]))
+        n = int(rng.integers(1, 1 << 24)) if A > 1 else int(rng.integers(1, 5000))
+        U = -(-n // A)
+        K = int(rng.integers(1, min(U, 64) + 1))
+        assert G.plan_parts(n, K, A, plan="balanced") == oracle.make_parts_balanced(n, K, A), (n, K, A)
 
 
 def test_plan_parts_errors(G):
@@ -239,6 +262,22 @@ def test_ring_bytes_required(G):
                 best = max(best, 3 * al(4 * (hi - lo)) + al(2 * (hi if i < K - 1 else 0)))
         assert G.ring_bytes_required(n, kmin, kmax, A, R) == R * best
     assert G.ring_bytes_required(0, 1, 4) == 0 and G.ring_bytes_required(100, 5, 4) == 0
+
+
+def test_ring_bytes_required_balanced(G):
+    # the same rule over the balanced plans; a smaller ring wherever the plan lowers V_max
+    al = lambda x: (x + 255) // 256 * 256
+    for n, kmin, kmax, A, R in [(124_439_808, 8, 8, 1024, 2), (3_253_966_336, 2, 16, 1024, 2), (1000, 1, 4, 8, 1)]:
+        best = 0
+        for K in range(kmin, kmax + 1):
+            parts = oracle.make_parts_balanced(n, K, A)
+            for i, (lo, hi) in enumerate(parts):
+                best = max(best, 3 * al(4 * (hi - lo)) + al(2 * (hi if i < K - 1 else 0)))
+        got = G.ring_bytes_required(n, kmin, kmax, A, R, plan="balanced")
+        assert got == R * best
+        assert got <= G.ring_bytes_required(n, kmin, kmax, A, R)
+    assert G.ring_bytes_required(124_439_808, 8, 8, 1024, 2, plan="balanced") < \
+        0.8 * G.ring_bytes_required(124_439_808, 8, 8, 1024, 2)
 
 
 # ---------------------------------------------------------------- a3 drain verification checksum
