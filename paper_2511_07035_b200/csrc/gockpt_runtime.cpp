@@ -1462,8 +1462,18 @@ gck_status gck_submit(gck_ctx *c, uint32_t part, const gck_step_args *a, void *s
         f.sm = reinterpret_cast<float *>(slot + L.off_m);
         f.sv = reinterpret_cast<float *>(slot + L.off_v);
         f.sg = reinterpret_cast<uint16_t *>(slot + L.off_g);
+        // a3 verification folded into the pack where the kernel supports it: the pack warp checksums
+        // the bytes it stores (into dsum[i-1], zeroed here on the compute stream)
+        if (c->verify && c->fault_drop != i) {
+            f.ck = c->dsum + (uint64_t)(i - 1) * 8;
+            if (cudaMemsetAsync(f.ck, 0, 8 * sizeof(unsigned long long), s) != cudaSuccess) {
+                cudaGetLastError();
+                f.ck = nullptr;
+            }
+        }
     }
-    int le = gck::launch_fused(f, ck_ok, s, c->num_sms);
+    bool ck_folded = false;
+    int le = gck::launch_fused(f, ck_ok, s, c->num_sms, &ck_folded);
     if (le) return c->cuda_fail((cudaError_t)le, "fused kernel launch");
     c->stats.gpu_launches++;
     c->stats.session_steps++;
@@ -1483,7 +1493,13 @@ gck_status gck_submit(gck_ctx *c, uint32_t part, const gck_step_args *a, void *s
         c->stream_worker_failed();
         return GCK_E_ABORTED;
     }
-    if (c->fault_drop != i) {
+    if (c->fault_drop != i && ck_folded) {  // the pack's checksums -> the pinned mirror, behind the pack
+        if (cudaMemcpyAsync(c->hsum + (uint64_t)(i - 1) * 8, c->dsum + (uint64_t)(i - 1) * 8,
+                            8 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, c->d2h) != cudaSuccess) {
+            c->abort_session(cudaGetLastError(), "drain verification checksum copy");
+            return GCK_E_ABORTED;
+        }
+    } else if (c->fault_drop != i) {
         const void *src[4] = {slot, slot + L.off_m, slot + L.off_v, slot + L.off_g};
         const uint64_t pe = hi - lo, bytes[4] = {pe * 4, pe * 4, pe * 4, ghi * 2};
         if (enqueue_checksum(c, i, src, bytes, ghi ? 4 : 3, 0) != GCK_OK) {

@@ -24,6 +24,9 @@ struct FusedArgs {
     uint64_t lo, hi, ghi;
     float *sp, *sm, *sv;
     uint16_t *sg;
+    // drain verification folded into the pack (nullable): (A, B) of sections master, m, v, gradient
+    // at ck[2s], ck[2s+1], accumulated (zeroed by the caller) over the bytes the pack stores
+    unsigned long long *ck;
 };
 
 // Arguments of one replay launch (a5, GPU).
@@ -58,7 +61,9 @@ struct ZcArgs {
 };
 
 // Launchers (kernels.cu). Return the cudaError_t as int (0 = success).
-int launch_fused(const FusedArgs &a, bool pack, void *stream, int num_sms);
+// *ck_folded (nullable) = true when the launched kernel accumulated a.ck (the bulk-store kernel's
+// pack warp); false when the caller still has to checksum the slot with launch_checksum.
+int launch_fused(const FusedArgs &a, bool pack, void *stream, int num_sms, bool *ck_folded = nullptr);
 int launch_replay(const ReplayArgs &a, void *stream, int num_sms);
 int launch_zerocopy_drain(const ZcArgs &a, int ctas, void *stream);
 int launch_generate(int kind, int mode, uint64_t seed, uint64_t step, uint64_t offset, uint64_t n,

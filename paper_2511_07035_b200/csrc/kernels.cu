@@ -446,6 +446,11 @@ __global__ void __launch_bounds__((kCW + 3) * 32, 1) fused_adamw_pack_tmast_kern
     }
     const RecF r = to_recf(a.rec);
     const int c = threadIdx.x;
+    // drain verification folded into the pack (a.ck): each consumer checksums the pre-update words
+    // it loaded that the pack stores (state words of [lo, hi), gradient words of [0, ghi)); a vector
+    // of 4 words at section index k0 adds sum to A and (k0+1) sum + (w1 + 2 w2 + 3 w3) to B
+    const bool ck = PACK && a.ck != nullptr;
+    uint64_t ca[4] = {0, 0, 0, 0}, cb[4] = {0, 0, 0, 0};
     uint32_t k = 0;
     for (uint64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x, ++k) {
         const int s = k % kStages;
@@ -474,6 +479,30 @@ __global__ void __launch_bounds__((kCW + 3) * 32, 1) fused_adamw_pack_tmast_kern
         if (lane == 0) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             mbar_arrive(&empty[s]);
+        }
+        if (ck) {
+            const uint64_t base = tile * kTile;
+#pragma unroll
+            for (int q = 0; q < kQ; ++q) {
+                const uint64_t e0 = base + 4 * (uint64_t)(c + q * kThreads);  // boundaries are multiples of 8
+                if (e0 < a.ghi) {
+                    const uint64_t sum = (uint64_t)gq[q].x + gq[q].y;
+                    ca[3] += sum;
+                    cb[3] += (e0 / 2 + 1) * sum + gq[q].y;
+                }
+                if (e0 >= a.lo && e0 < a.hi) {
+                    const uint64_t k1 = e0 - a.lo + 1;
+                    const float4 *vs[3] = {&pq[q], &mq[q], &vq[q]};
+#pragma unroll
+                    for (int sec = 0; sec < 3; ++sec) {
+                        const uint32_t w0 = __float_as_uint(vs[sec]->x), w1 = __float_as_uint(vs[sec]->y),
+                                       w2 = __float_as_uint(vs[sec]->z), w3 = __float_as_uint(vs[sec]->w);
+                        const uint64_t sum = (uint64_t)w0 + w1 + w2 + w3;
+                        ca[sec] += sum;
+                        cb[sec] += k1 * sum + ((uint64_t)w1 + 2 * (uint64_t)w2 + 3 * (uint64_t)w3);
+                    }
+                }
+            }
         }
         // compute, then write the tile's results into output buffer o once the store warp has
         // finished reading its previous contents
@@ -507,6 +536,7 @@ __global__ void __launch_bounds__((kCW + 3) * 32, 1) fused_adamw_pack_tmast_kern
     }
     // ragged tail [n_tiles*kTile, n): block 0's consumers, plain loads and stores
     if (blockIdx.x == 0) {
+        uint64_t *ta = ca, *tb = cb;  // the tail's packed bytes join this thread's folded checksum
         for (uint64_t e = n_tiles * kTile + (uint64_t)c; e < a.n; e += kThreads) {
             float p = a.p[e], m = a.m[e], v = a.v[e];
             const uint32_t g = a.g[e];
@@ -515,8 +545,20 @@ __global__ void __launch_bounds__((kCW + 3) * 32, 1) fused_adamw_pack_tmast_kern
                     a.sp[e - a.lo] = p;
                     a.sm[e - a.lo] = m;
                     a.sv[e - a.lo] = v;
+                    const uint64_t w1 = e - a.lo + 1;
+                    const uint32_t ws[3] = {__float_as_uint(p), __float_as_uint(m), __float_as_uint(v)};
+#pragma unroll
+                    for (int sec = 0; sec < 3; ++sec) {
+                        ta[sec] += ws[sec];
+                        tb[sec] += w1 * ws[sec];
+                    }
                 }
-                if (e < a.ghi) a.sg[e] = (uint16_t)g;
+                if (e < a.ghi) {
+                    a.sg[e] = (uint16_t)g;
+                    const uint64_t half = (uint64_t)g << (16 * (e & 1));  // this element's share of word e/2
+                    ta[3] += half;
+                    tb[3] += (e / 2 + 1) * half;
+                }
             }
             if (!skip) {
                 adamw_elem_fast(p, m, v, g, r);
@@ -525,6 +567,25 @@ __global__ void __launch_bounds__((kCW + 3) * 32, 1) fused_adamw_pack_tmast_kern
                 a.v[e] = v;
             }
             if (a.out) a.out[e] = (uint16_t)(pack_bf16x2(p, 0.f) & 0xFFFFu);
+        }
+    }
+    if (ck) {
+#pragma unroll
+        for (int sec = 0; sec < 4; ++sec) {
+#pragma unroll
+            for (int d = 16; d > 0; d >>= 1) {
+                ca[sec] += __shfl_xor_sync(0xFFFFFFFFu, ca[sec], d);
+                cb[sec] += __shfl_xor_sync(0xFFFFFFFFu, cb[sec], d);
+            }
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int sec = 0; sec < 4; ++sec) {
+                if (ca[sec] | cb[sec]) {
+                    atomicAdd(a.ck + 2 * sec, (unsigned long long)ca[sec]);
+                    atomicAdd(a.ck + 2 * sec + 1, (unsigned long long)cb[sec]);
+                }
+            }
         }
     }
 }
@@ -882,8 +943,9 @@ int fused_impl_default() {
     return 0;
 }
 
-int launch_fused(const FusedArgs &a, bool pack, void *stream, int num_sms) {
+int launch_fused(const FusedArgs &a, bool pack, void *stream, int num_sms, bool *ck_folded) {
     cudaStream_t s = static_cast<cudaStream_t>(stream);
+    if (ck_folded) *ck_folded = false;
     const int impl = fused_impl_default();
     const bool aligned = ((reinterpret_cast<uintptr_t>(a.p) | reinterpret_cast<uintptr_t>(a.m) |
                            reinterpret_cast<uintptr_t>(a.v) | reinterpret_cast<uintptr_t>(a.g)) & 15u) == 0;
@@ -891,6 +953,7 @@ int launch_fused(const FusedArgs &a, bool pack, void *stream, int num_sms) {
     // default for n >= 2^18: the bulk-store variant (3 input + 3 output stages); GCK_FUSED_IMPL=t
     // selects the STG-store TMA kernel, s the plain grid-stride kernel
     if (aligned && out_aligned && (impl == 3 ? a.n >= 2048 : (impl == 0 && a.n >= kTmaMinElems))) {
+        if (ck_folded) *ck_folded = pack && a.ck != nullptr;
         const char *e = getenv("GCK_TMAST_CFG");
         int st = 3, o = 3, cw = 16;
         if (e) sscanf(e, "%d,%d,%d", &st, &o, &cw);
