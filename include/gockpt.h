@@ -133,8 +133,10 @@ typedef struct {
                                P:401: "28 cores per process, same NUMA domain". */
     uint32_t stream_buffers; /* GCK_REPLAY_STREAM: gradient slice buffers B (0 -> min(4, k_max - 1)); ignored
                                 otherwise */
-    int32_t verify_drain;   /* 1: verify every drained slice (a3) — a checksum kernel reads each section on
-                               the D2H stream right before its copy (the bytes the copy reads), the host
+    int32_t verify_drain;   /* 1: verify every drained slice (a3) — the device checksums the staged bytes (ring
+                               staging with the bulk-store fused kernel: folded into the pack, from the words
+                               the kernel stores; otherwise a checksum kernel reads each section on the D2H
+                               stream right before its copy), the host
                                recomputes the checksum of the landed bytes before the replay uses them
                                (A = sum w_i, B = sum (i+1) w_i mod 2^64 over 32-bit words); a mismatch
                                voids the session with GCK_E_CORRUPT. 0: no verification */
