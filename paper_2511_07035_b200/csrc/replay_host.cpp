@@ -250,6 +250,21 @@ gck_status replay_host_impl(const gck_step_record *recs, uint32_t K, const uint6
             uint64_t sa[3] = {0, 0, 0}, sb[3] = {0, 0, 0}, ga[GCK_K_LIMIT] = {}, gb[GCK_K_LIMIT] = {};
             for (uint64_t b0 = tk.a; b0 < tk.b; b0 += kBlock) {
                 const int cnt = (int)std::min<uint64_t>(kBlock, tk.b - b0);
+                if (sums && b0 + kBlock < tk.b) {
+                    // the checksum pass below is the block's first touch and has little compute to hide
+                    // DRAM latency behind: prefetch the next block's state and gradient lines now, so
+                    // their misses overlap this block's updates (the replay alone needs no prefetch:
+                    // its first touch is inside the update arithmetic)
+                    const uint64_t b1 = b0 + kBlock, c1 = std::min<uint64_t>(kBlock, tk.b - b1);
+                    for (uint64_t o = 0; o < c1 * 4; o += 64) {
+                        _mm_prefetch(reinterpret_cast<const char *>(p + b1) + o, _MM_HINT_T0);
+                        _mm_prefetch(reinterpret_cast<const char *>(m + b1) + o, _MM_HINT_T0);
+                        _mm_prefetch(reinterpret_cast<const char *>(v + b1) + o, _MM_HINT_T0);
+                    }
+                    for (uint32_t i = tk.j; i + 1 < K; ++i)
+                        for (uint64_t o = 0; o < c1 * 2; o += 64)
+                            _mm_prefetch(reinterpret_cast<const char *>(glog[i] + b1) + o, _MM_HINT_T0);
+                }
                 if (sums) {  // the block's landed bytes, before the first update overwrites them (in L1)
                     const float *sec[3] = {p + b0, m + b0, v + b0};
                     const uint64_t w0 = b0 - lo[tk.j];  // word index inside the part's sections
