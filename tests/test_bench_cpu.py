@@ -72,6 +72,7 @@ def test_reference_and_gpu_arm_share_the_config():
     bench.resolve(a)
     c1 = bench.config_dict(a, 1)
     assert dict(c1, K=8) == c1 and c1["fb_tflop_per_step"] > 10 and c1["n_per_rank"] == 124_439_808
+    assert c1["plan"] == "equal"                                   # the partition plan is part of the workload key
 
 
 def test_resolve_shards():
