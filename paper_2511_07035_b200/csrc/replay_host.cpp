@@ -121,8 +121,10 @@ void flush_plain(const char *a, const char *e) {
 uint64_t evict_budget() {
     static const uint64_t budget = [] {
         if (const char *e = getenv("GCK_EVICT_BYTES")) return (uint64_t)strtoull(e, nullptr, 10);
+        // the private caches that can hold arena lines are those of the cores this process may run on
+        // (its affinity mask: on a multi-GPU host each rank's replay threads are bound to a subset)
         const long l2 = sysconf(_SC_LEVEL2_CACHE_SIZE), l3 = sysconf(_SC_LEVEL3_CACHE_SIZE);
-        const long cpus = sysconf(_SC_NPROCESSORS_ONLN);
+        const long cpus = default_threads();
         uint64_t cached = (l2 > 0 && cpus > 0 ? (uint64_t)l2 * (uint64_t)cpus : 0) + (l3 > 0 ? (uint64_t)l3 : 0);
         if (cached == 0) cached = 128ull << 20;  // sysconf without cache data: a generous guess
         return std::max<uint64_t>(2 * cached, 16ull << 20);
