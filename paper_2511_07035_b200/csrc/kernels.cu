@@ -691,8 +691,8 @@ __global__ void __launch_bounds__(256) replay_kernel(const ReplayPlan a) {
 // covers 512 contiguous bytes (replay_kernel's 8-consecutive-element threads touch every 32-B sector
 // twice, half of it each time: 1.6x the L1 sector lookups, more long-scoreboard waits). 2-3% faster
 // (GPT-2/K=8 645 vs 661 us, K=4 432 vs 447-466 us; ncu L1 load sectors 68M = the algorithmic bytes).
-template <bool kUnitGs, bool kAllFast>
-__global__ void __launch_bounds__(256, 4) replay_coalesced_kernel(const ReplayPlan a) {
+template <bool kUnitGs, bool kAllFast, int kBlk>
+__global__ void __launch_bounds__(kBlk, 1024 / kBlk) replay_coalesced_kernel(const ReplayPlan a) {
     __shared__ RecP srec[GCK_K_LIMIT];
     for (uint32_t q = threadIdx.x; q < a.nact; q += blockDim.x) srec[q].f = to_recf(a.rec[q]);
     __syncthreads();
@@ -1061,12 +1061,15 @@ int launch_replay(const ReplayArgs &a, void *stream, int num_sms) {
         for (uint32_t i = 0; i + 1 < a.K; ++i) b256 = b256 && ((a.hi[i] & 255u) == 0);
         const char *ce = getenv("GCK_REPLAY_COALESCED");  // "0": the 8-consecutive-element form
         if (b256 && !(ce && ce[0] == '0')) {
-            const unsigned g2 = grid;
+            // 128-thread CTAs, twice as many (the same threads in flight): the finer-grained CTAs let
+            // the scheduler mix FP-heavy and HBM-heavy parts on an SM more evenly (GPT-2/K=8 599 vs 611 us,
+            // K=4 and 7B/K=8 unchanged; r02_replay_blk*.jsonl)
+            const unsigned g2 = grid * 2;
             switch ((unit_gs ? 2 : 0) | (all_fast(rp) ? 1 : 0)) {
-                case 3: replay_coalesced_kernel<true, true><<<g2, 256, 0, s>>>(rp); break;
-                case 2: replay_coalesced_kernel<true, false><<<grid, 256, 0, s>>>(rp); break;
-                case 1: replay_coalesced_kernel<false, true><<<grid, 256, 0, s>>>(rp); break;
-                default: replay_coalesced_kernel<false, false><<<grid, 256, 0, s>>>(rp); break;
+                case 3: replay_coalesced_kernel<true, true, 128><<<g2, 128, 0, s>>>(rp); break;
+                case 2: replay_coalesced_kernel<true, false, 128><<<g2, 128, 0, s>>>(rp); break;
+                case 1: replay_coalesced_kernel<false, true, 128><<<g2, 128, 0, s>>>(rp); break;
+                default: replay_coalesced_kernel<false, false, 128><<<g2, 128, 0, s>>>(rp); break;
             }
             return (int)cudaGetLastError();
         }
