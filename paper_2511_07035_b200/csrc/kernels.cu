@@ -1051,7 +1051,8 @@ int launch_replay(const ReplayArgs &a, void *stream, int num_sms) {
     ReplayPlan rp;
     bool unit_gs = false;
     if (replay_plan(a, &rp, &unit_gs)) {
-        // 64 CTAs per SM (~5 grid-stride iterations per thread at GPT-2 size): the CTA scheduler then
+        // 64 CTAs per SM of 256 threads (~5 grid-stride iterations per thread at GPT-2 size; the
+        // coalesced kernel runs the same threads as 128-thread CTAs, below): the CTA scheduler then
         // keeps starting fresh CTAs on every SM while others are still on earlier parts, which mixes
         // the FP-heavy first parts with the HBM-heavy last parts on each SM (r02_replay11.jsonl: 8 per SM
         // 644 us, 16: 618, 64: 611 at GPT-2/K=8; K=4 444 -> 408 us; one wave (4): 695 us)
